@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""bench.py -- the VBDR hot path on B200 (one JSON line on rank 0).
+
+A step is one slice of the method over one batch of synthetic input:
+    vbdr_scan_slice (Np pairs) -> [N>1: allreduce(MAX) merge] -> vbdr_slide
+    -> vbdr_estimate (all H hosts)
+on BASELINE.json configs[1] ('caida': 5M pairs/slice, 500k Zipf hosts, m=128,
+2^22 physical BDRs, k=5) unless --config says otherwise.
+
+value   = pairs/s of whole steps (Mpairs/s), inputs resident in HBM, L2 flushed
+          before every step, device time from CUDA events, max over ranks.
+e2e     = the same through the host-buffer C ABI entry points (pinned host pairs
+          copied in, estimates copied out, inside the timed region).
+Under torchrun (N>1) each rank scans 1/N of every slice's pairs, the stamp
+arrays merge by NCCL allreduce(MAX), and each rank estimates 1/N of the hosts.
+
+--impl reference times the oracle (oracle/, single thread, host cores) on a
+1/32-scale replica of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+# BASELINE.json workloads -> (m, k, n_phys)
+WORKLOADS = {
+    "tiny": dict(m=32, k=4, n_phys=1 << 12),
+    "caida": dict(m=128, k=5, n_phys=1 << 22),
+    "10G": dict(m=256, k=10, n_phys=1 << 26),
+    "bigwin": dict(m=256, k=60, n_phys=1 << 28),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="vbdr", choices=["vbdr", "reference"])
+    ap.add_argument("--config", default="caida", choices=list(WORKLOADS))
+    ap.add_argument("--layout", default="fast", choices=["fast", "packed"])
+    ap.add_argument("--scan-mode", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--flush-mib", type=int, default=512)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes_per_bdr(layout: str, words: int) -> int:
+    """Slide kernel, per physical BDR: read sr (4 B, fast only), read+write W
+    packed DRV words (8 W B), write the register value (1 B).  DESIGN.md s.6."""
+    return (4 if layout == "fast" else 0) + 8 * words + 1
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        self.path = os.path.join("/tmp", f"vbdr_clocks_{os.getpid()}.csv")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sms, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sms:
+            return None
+        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+# ------------------------------------------------------------- reference arm
+def oracle_slice_time(tr: synth.TraceConfig, wl: dict, seconds: float, min_slices: int,
+                      scale: int):
+    """Time the oracle (serial VBDR, single thread) on whole slices of a
+    1/scale replica of the workload.  Returns (seconds per slice, pairs/slice,
+    slices, sample description)."""
+    import oracle
+    oracle.lib()
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except Exception:
+        pass
+    n_phys = wl["n_phys"] // scale
+    np_pairs = tr.pairs_per_slice // scale
+    hosts_n = max(1, tr.hosts // scale)
+    b = wl["m"].bit_length() - 1
+    cfg = oracle.PoolConfig(b=b, k=wl["k"], z=n_phys)
+    pool = oracle.Pool(cfg, "serial")
+    hosts = tr.host_ids()[:hosts_n]
+    slices = [synth.generate(tr, t, 0, np_pairs) for t in range(min(4, max(min_slices, 1)))]
+    pool.slice(slices[0])  # warm: touches the whole pool once
+    times = []
+    t_all = time.perf_counter()
+    i = 0
+    while (time.perf_counter() - t_all < seconds) or len(times) < min_slices:
+        pairs = slices[i % len(slices)]
+        t0 = time.perf_counter()
+        pool.begin_slice()
+        pool.scan(pairs)
+        pool.end_slice()
+        pool.estimate(pool.readout(), hosts)
+        times.append(time.perf_counter() - t0)
+        i += 1
+    sample = (f"oracle serial VBDR, 1 thread, {'full-size' if scale == 1 else f'1/{scale}-scale'} "
+              f"{tr.name} slices: {np_pairs} pairs scanned + {n_phys} BDRs closed + {hosts_n} "
+              f"hosts estimated per slice, {len(times)} slices")
+    return float(np.mean(times)), np_pairs, len(times), sample
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    tr = synth.CONFIGS[args.config]
+    wl = WORKLOADS[args.config]
+    scale = 32 if args.config != "tiny" else 1
+    import oracle
+    b = wl["m"].bit_length() - 1
+    cfg = oracle.PoolConfig(b=b, k=wl["k"], z=wl["n_phys"] // scale)
+    pool = oracle.Pool(cfg, "serial")
+    np_pairs = tr.pairs_per_slice // scale
+    hosts = tr.host_ids()[:max(1, tr.hosts // scale)]
+    slices = [synth.generate(tr, t, 0, np_pairs) for t in range(4)]
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except Exception:
+        pass
+
+    def step(i):
+        pool.begin_slice()
+        pool.scan(slices[i % 4])
+        pool.end_slice()
+        pool.estimate(pool.readout(), hosts)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(i)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = np_pairs / dt / 1e6
+    sample = (f"oracle serial VBDR, 1 thread, 1/{scale}-scale {args.config}: {np_pairs} pairs + "
+              f"{cfg.z} BDRs + {len(hosts)} hosts per step")
+    line = {
+        "impl": "reference", "metric": "IP pairs scanned per second through whole slices "
+        "(scan + slide + estimate)", "value": round(value, 4), "unit": "Mpairs/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": args.config, "layout": "oracle-serial", **wl,
+                   "pairs_per_slice": tr.pairs_per_slice, "hosts": tr.hosts,
+                   "sample_scale": f"1/{scale}"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mpairs/s", "cores": 1,
+                         "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "Mpairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_vbdr(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1810_13132_b200 import VBDR, merge_stamps, shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+
+    tr = synth.CONFIGS[args.config]
+    wl = WORKLOADS[args.config]
+    pool = VBDR(wl["m"], wl["k"], wl["n_phys"], layout=args.layout, scan_mode=args.scan_mode,
+                device=dev)
+    info = pool.info()
+    p0, p1 = shard_range(tr.pairs_per_slice, rank, world)
+    h0, h1 = shard_range(tr.hosts, rank, world)
+    n_local = p1 - p0
+    gen = synth.DeviceTrace(tr, dev)
+    n_inputs = min(args.steps + args.warmup, 16)
+    inputs = []
+    for t in range(n_inputs):
+        buf = torch.empty(2 * n_local, dtype=torch.int32, device=dev)
+        gen.generate_into(buf, t, start=p0)
+        inputs.append(buf)
+    hosts_all = tr.host_ids()
+    hosts = torch.from_numpy(hosts_all[h0:h1].view(np.int32)).to(dev)
+    est_out = torch.empty(h1 - h0, dtype=torch.float64, device=dev)
+    flush = torch.empty(args.flush_mib << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(i, evs=None):
+        x = inputs[i % n_inputs]
+        if evs:
+            evs[0].record(stream)
+        pool.scan_slice(x)
+        if evs:
+            evs[1].record(stream)
+        if group is not None:
+            merge_stamps(pool, group)
+        if evs:
+            evs[2].record(stream)
+        pool.slide()
+        if evs:
+            evs[3].record(stream)
+        pool.estimate(hosts, out=est_out)
+        if evs:
+            evs[4].record(stream)
+
+    # warm-up
+    for i in range(args.warmup):
+        flush.fill_(i & 0xFF)
+        step(i)
+    barrier()
+
+    # ---- device-resident timed region
+    clocks = ClockSampler(local) if rank == 0 else None
+    events = [[E() for _ in range(5)] for _ in range(args.steps)]
+    launches0 = pool.info()["launches"]
+    barrier()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)  # L2 flush (> 126 MB L2), outside the step events
+        step(args.warmup + i, events[i])
+    barrier()
+    launches = pool.info()["launches"] - launches0
+    clk = clocks.stop() if clocks else None
+    ms = np.array([[ev[j].elapsed_time(ev[j + 1]) for j in range(4)] for ev in events])
+    step_ms_local = ms.sum(axis=1)
+    local_total = float(step_ms_local.sum())
+    per_kernel_local = ms.mean(axis=0)  # scan, merge, slide, estimate
+    if world > 1:
+        t = torch.tensor([local_total, *per_kernel_local.tolist()], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t[0])
+        per_kernel = t[1:].cpu().numpy()
+    else:
+        total_ms = local_total
+        per_kernel = per_kernel_local
+    ms_per_step = total_ms / args.steps
+    value = tr.pairs_per_slice / (ms_per_step * 1e-3) / 1e6
+
+    # ---- end to end through the host-buffer C ABI entry points
+    e2e = None
+    if not args.no_e2e:
+        h_inputs = [inputs[i].cpu().pin_memory() for i in range(min(n_inputs, 4))]
+        h_hosts = torch.from_numpy(hosts_all[h0:h1].view(np.int32)).pin_memory()
+        h_out = torch.empty(h1 - h0, dtype=torch.float64).pin_memory()
+        stage = torch.empty(2 * min(n_local, 1 << 21), dtype=torch.int32, device=dev)
+        hstage = torch.empty(max(h1 - h0, 1), dtype=torch.int32, device=dev)
+        ostage = torch.empty(max(h1 - h0, 1), dtype=torch.float64, device=dev)
+
+        def e2e_step(i):
+            pool.scan_slice_host(h_inputs[i % len(h_inputs)], stage)
+            if group is not None:
+                merge_stamps(pool, group)
+            pool.slide()
+            pool.estimate_host(h_hosts, hstage, ostage, h_out)
+
+        for i in range(3):
+            e2e_step(i)
+        barrier()
+        ev = [(E(), E()) for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            e2e_step(i)
+            ev[i][1].record(stream)
+        barrier()
+        e2e_ms = sum(a.elapsed_time(b) for a, b in ev)
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t[0])
+        e2e = {"value": round(tr.pairs_per_slice / (e2e_ms / args.steps * 1e-3) / 1e6, 3),
+               "unit": "Mpairs/s", "h2d_bytes_per_step": 8 * n_local * world + 4 * tr.hosts,
+               "d2h_bytes_per_step": 8 * tr.hosts,
+               "ms_per_step": e2e_ms / args.steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel
+    hbm, hbm_src = peaks()
+    names = ["scan", "merge", "slide", "estimate"]
+    kern = {n: float(v) for n, v in zip(names, per_kernel)}
+    slide_bytes = algorithmic_bytes_per_bdr(args.layout, info["words"]) * wl["n_phys"]
+    slide_gbs = slide_bytes / (kern["slide"] * 1e-3) / 1e9
+    pairs_local = n_local
+    kernels = {
+        "scan": {"ms": kern["scan"], "mpairs_s": pairs_local / (kern["scan"] * 1e-3) / 1e6,
+                 "bound": "l2_atomic", "bytes_per_pair": 8},
+        "merge": {"ms": kern["merge"]},
+        "slide": {"ms": kern["slide"], "bound": "hbm", "bytes": slide_bytes,
+                  "achieved_gbs": slide_gbs, "frac": slide_gbs / hbm},
+        "estimate": {"ms": kern["estimate"], "hosts": h1 - h0,
+                     "gathers_per_s": (h1 - h0) * wl["m"] / (kern["estimate"] * 1e-3)},
+    }
+    dominant = max(("scan", "slide", "estimate"), key=lambda n: kern[n])
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"{args.config}/{args.layout}/{dominant}")
+        except Exception:
+            traffic = None
+    if dominant == "slide":
+        roof = {"kernel": "slide", "bound": "hbm", "achieved": round(slide_gbs, 1),
+                "peak": hbm, "unit": "GB/s", "frac": round(slide_gbs / hbm, 4), "traffic": traffic,
+                "peak_source": hbm_src}
+    else:
+        # scan / estimate: the algorithmic DRAM bytes (8 B per pair in, 4 B per
+        # host in + 8 B out) -- a strict HBM roofline; their real limit is the
+        # L2 random-access rate (DESIGN.md s.6)
+        if dominant == "scan":
+            byts = 8 * pairs_local
+        else:
+            byts = 12 * (h1 - h0)
+        ach = byts / (kern[dominant] * 1e-3) / 1e9
+        roof = {"kernel": dominant, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
+                "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": traffic,
+                "peak_source": hbm_src}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        sec, npairs, nsl, sample = oracle_slice_time(tr, wl, args.cpu_seconds, 2, 1)
+        cpu = {"value": round(npairs / sec / 1e6, 4), "unit": "Mpairs/s", "cores": 1,
+               "kind": "oracle", "sample": sample}
+
+    line = {
+        "metric": "IP pairs scanned per second through whole slices (scan + slide + estimate)",
+        "value": round(value, 3), "unit": "Mpairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": args.config, "layout": args.layout, **wl,
+                   "pairs_per_slice": tr.pairs_per_slice, "hosts": tr.hosts,
+                   "parallelism": f"pairs+hosts sharded x{world}, allreduce(MAX) merge",
+                   "l2": f"flushed before every step ({args.flush_mib} MiB write)",
+                   "scan_mode": args.scan_mode},
+        "scan_mpairs_s": round(tr.pairs_per_slice / (kern["scan"] * 1e-3) / 1e6, 2),
+        "slide_ms": round(kern["slide"], 5), "estimate_ms": round(kern["estimate"], 5),
+        "merge_ms": round(kern["merge"], 5),
+        "kernels": kernels,
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_vbdr(args)
+
+
+if __name__ == "__main__":
+    main()

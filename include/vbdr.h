@@ -1,0 +1,190 @@
+/*
+ * vbdr.h -- C ABI of the B200-native VBDR hot path (libvbdr.so).
+ *
+ * VBDR: Jie Xu, "Cardinalities estimation under sliding time window by sharing
+ * HyperLogLog Counter", arXiv 1810.13132.  Citations "PAPER.md:N" are lines of
+ * the paper text; "R#n" rows of the reading ledger in DESIGN.md section 3.
+ *
+ * One slice of the method is
+ *     vbdr_scan_slice (any number of times)  -> [merge, N > 1] -> vbdr_slide
+ *     -> vbdr_estimate (any number of times)
+ *
+ * Conventions (all entry points):
+ *  - Pointers prefixed d_ are device pointers, h_ host pointers.  The CALLER
+ *    owns all device memory (the state buffer, pair batches, host lists,
+ *    outputs) and keeps it alive until the stream work that uses it is done;
+ *    the library stores only pointers and the configuration.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Calls are stream-ordered and asynchronous unless marked SYNC.
+ *  - Argument errors are reported synchronously (VBDR_EINVAL / VBDR_ERANGE /
+ *    VBDR_ESTATE) before anything is launched; a CUDA error (including an
+ *    asynchronous fault from earlier work) is returned as VBDR_ECUDA.  The
+ *    text of the last error of a handle is vbdr_last_error(h).
+ *  - One handle per device and host thread; a handle is not thread-safe.
+ *  - IP addresses are host-order u32 (a.b.c.d -> a<<24|b<<16|c<<8|d, R#21).
+ */
+#ifndef VBDR_H
+#define VBDR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vbdr vbdr_t; /* opaque handle */
+
+typedef enum {
+    VBDR_OK = 0,
+    VBDR_EINVAL = -1, /* bad argument or configuration                       */
+    VBDR_ERANGE = -2, /* size out of the supported range                     */
+    VBDR_ESTATE = -3, /* call not valid in the handle's current state        */
+    VBDR_ENOMEM = -4, /* state buffer too small / host allocation failed     */
+    VBDR_ECUDA = -5   /* CUDA runtime error (text in vbdr_last_error)        */
+} vbdr_status;
+
+typedef enum {
+    /* Stamp word sr[j] = (T << 5) | max rank of the open slice (the paper's
+     * nowLBP1, made race-free with atomicMax)
+     * plus the packed DRV.  VBDR-serial / VBDR-gfast semantics (Alg.1/4 and
+     * Alg.6/7): one rank recorded per register-slice. */
+    VBDR_LAYOUT_FAST = 0,
+    /* Packed DRV only, every rank recorded with atomicAnd (Alg.9)
+     * and aged at the slide (Alg.8 hoisted).  VBDR-gsmall
+     * semantics, the memory-efficient variant (Table 1). */
+    VBDR_LAYOUT_PACKED = 1
+} vbdr_layout;
+
+typedef struct {
+    /* m: virtual BDRs per host -- the paper's g = 2^b.  Power of
+     * two, 2 <= m, 2*m <= n_phys (R#15), n_phys / m <= 2^21 (exact sums). */
+    uint32_t m;
+    /* k: window length in slices, W(t,k).  1 <= k. */
+    uint32_t k;
+    /* n_phys: physical BDRs in the shared pool BDRP -- the paper's z
+     * (PAPER.md:152, 164).  Power of two, 4 <= n_phys <= 2^32. */
+    uint64_t n_phys;
+    /* seed_a0 / seed_a1: the paper's A0 (physical index, Alg.3)
+     * and A1 (opposite host, Alg.4).  Defaults (R#7):
+     * 0x5EED0001 / 0x5EED0002 when both are 0. */
+    uint32_t seed_a0;
+    uint32_t seed_a1;
+    /* zbits: DR width z.  0 = ceil(log2(k+1)), plus one for
+     * VBDR_LAYOUT_PACKED when k = 2^zbits - 1 (R#2).  Explicit values must
+     * satisfy 2^zbits - 1 >= k (packed: 2^zbits - 2 >= k); 1 <= zbits <= 10. */
+    uint32_t zbits;
+    /* rank_cap: L, the number of ranks per BDR (R#3).  0 = 32 - log2(m);
+     * otherwise 1 <= rank_cap <= 32 - log2(m). */
+    uint32_t rank_cap;
+    /* layout: vbdr_layout. */
+    uint32_t layout;
+    /* scan_mode: 0 = default; 1 = plain atomic per pair; 2 = load-check, skip
+     * the atomic when the stored value already dominates; 3 = warp-aggregated
+     * atomics (__match_any_sync).  All modes give bit-identical state. */
+    uint32_t scan_mode;
+} vbdr_config;
+
+/* Derived sizes and the layout of the state buffer (byte offsets from the
+ * d_state pointer passed to vbdr_create). */
+typedef struct {
+    uint32_t b;            /* log2(m)                                         */
+    uint32_t L;            /* ranks per BDR                                   */
+    uint32_t zbits;        /* DR width in bits                                */
+    uint32_t fields;       /* F = floor(32 / zbits) DRs per 32-bit word       */
+    uint32_t words;        /* W = ceil(L / F) words per BDR                   */
+    uint32_t tick;         /* T = t + 1 of the open slice t                   */
+    uint64_t n_phys;
+    uint64_t slices_closed;/* number of vbdr_slide calls so far               */
+    uint64_t off_acc;      /* u64[4]: (S_tot, V_tot) for tick parity 0 and 1  */
+    uint64_t off_sr;       /* u32[n_phys] stamp words (LAYOUT_FAST only)      */
+    uint64_t off_drv;      /* u32[W][n_phys] packed DRV, plane-major          */
+    uint64_t off_regmax;   /* u8[n_phys] register values M[j] (Alg.2)         */
+    uint64_t state_bytes;  /* total bytes the state buffer needs              */
+    uint64_t launches;     /* kernels launched by this handle so far          */
+} vbdr_info_t;
+
+/* SYNC.  Bytes of device memory the caller must provide for this config. */
+vbdr_status vbdr_state_bytes(const vbdr_config *cfg, uint64_t *bytes);
+
+/* Validate cfg, bind the caller's state buffer (d_state, >= state_bytes,
+ * 256-byte aligned) and initialise it on `stream`: every DR to InitDR = 2^z-1
+ * (PAPER.md:94), stamps and registers to 0.  Slice t = 0 is open.
+ * *out receives the handle (host memory owned by the library). */
+vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes,
+                        void *stream, vbdr_t **out);
+
+/* Frees the handle and its streams/events; does not free d_state. */
+vbdr_status vbdr_destroy(vbdr_t *h);
+
+/* Scan n_pairs IP pairs of the open slice (Alg.4 lines 179-185 / Alg.9,
+ * PAPER.md:179-185, 288-292).  d_pairs is u32[2*n_pairs], interleaved
+ * (aip, bip), 16-byte aligned.  n_pairs = 0 is legal.  May be called any
+ * number of times per slice; the resulting state does not depend on the order
+ * or split of the pairs. */
+vbdr_status vbdr_scan_slice(vbdr_t *h, const uint32_t *d_pairs, uint64_t n_pairs,
+                            void *stream);
+
+/* Close the open slice t: age every DR, expire ranks older
+ * than k, record this slice's ranks (Alg.1 / Alg.8), materialise the register
+ * values M[j] = GetLBP1BDR (Alg.2) and the pool sums
+ * S_tot = sum_j 2^(L - M[j]) and V_tot = #{M[j] = 0}.  Opens slice t+1.
+ * Multi-GPU: the caller merges the stamp arrays of all ranks (elementwise
+ * max over sr, see vbdr_info) BEFORE this call. */
+vbdr_status vbdr_slide(vbdr_t *h, void *stream);
+
+/* Estimate |OP(aip, t, k)| (Definition 1) for n_hosts hosts
+ * over the window W(t-k+1..t) of the last closed slice: Alg.5 gather
+ * (PAPER.md:197-213), HyperLogLog harmonic mean with linear counting, vHLL
+ * noise subtraction (R#15, R#16), fp64.  d_hosts is
+ * u32[n_hosts], d_out f64[n_hosts].  Before the first slide every estimate
+ * is 0. */
+vbdr_status vbdr_estimate(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
+                          double *d_out, void *stream);
+
+/* Integer stage of vbdr_estimate for parity: per host S = sum_i
+ * 2^(L - M[pidx_i]) (u64) and V = #{M[pidx_i] = 0} (u32). */
+vbdr_status vbdr_host_sums(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
+                           uint64_t *d_S, uint32_t *d_V, void *stream);
+
+/* ---- host-buffer entry points (end-to-end path) ---------------------- */
+
+/* vbdr_scan_slice on HOST pairs: copies h_pairs (pinned for overlap) through
+ * the caller's device staging buffer d_stage (u32[2*stage_pairs], split in
+ * two halves) chunk by chunk, overlapping each chunk's host-to-device copy
+ * with the scan of the previous chunk.  Stream-ordered on `stream`; h_pairs
+ * must stay valid until that stream reaches this point. */
+vbdr_status vbdr_scan_slice_host(vbdr_t *h, const uint32_t *h_pairs, uint64_t n_pairs,
+                                 uint32_t *d_stage, uint64_t stage_pairs, void *stream);
+
+/* vbdr_estimate on HOST buffers: copies h_hosts into d_hosts_stage, runs the
+ * estimate into d_out_stage and copies the results into h_out.
+ * Stream-ordered; h_out is valid after the stream is synchronised. */
+vbdr_status vbdr_estimate_host(vbdr_t *h, const uint32_t *h_hosts, uint64_t n_hosts,
+                               uint32_t *d_hosts_stage, double *d_out_stage,
+                               double *h_out, void *stream);
+
+/* ---- introspection and SYNC exports (tests, snapshots) ---------------- */
+
+vbdr_status vbdr_info(const vbdr_t *h, vbdr_info_t *info);
+
+/* SYNC (synchronises `stream`).  DR ages as u16[n_phys * L], row j, column
+ * rho-1.  mode 0: the stored values (LAYOUT_FAST: the paper's DR values at
+ * the last boundary, R#1; LAYOUT_PACKED: values already aged for the open
+ * slice).  mode 1: canonical C_k[j][rho] = min(age, k) at the last boundary
+ * (DESIGN.md section 4). */
+vbdr_status vbdr_export_ages(vbdr_t *h, uint16_t *h_ages, int mode, void *stream);
+
+/* SYNC.  Register values M[j] (u8[n_phys]) of the last boundary. */
+vbdr_status vbdr_export_regmax(vbdr_t *h, uint8_t *h_regmax, void *stream);
+
+/* SYNC.  Pool sums of the last boundary. */
+vbdr_status vbdr_export_pool_sums(vbdr_t *h, uint64_t *h_S_tot, uint64_t *h_V_tot,
+                                  void *stream);
+
+const char *vbdr_last_error(const vbdr_t *h);
+const char *vbdr_status_string(vbdr_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VBDR_H */

@@ -1,0 +1,299 @@
+// k_scan_slide.cu -- pair-scan, slide/expire and init kernels of the VBDR hot
+// path for sm_100a.  DESIGN.md section 6 gives each kernel's roofline.
+//
+// Layout F ("fast", VBDR-serial/gfast semantics):
+//   sr[j] = (T << 5) | max rank seen by BDR j in slice T-1 -- the paper's
+//   nowLBP1 with the slice tick folded in, so it never
+//   needs clearing; the parallel max is an atomicMax (the race of PAPER.md:220
+//   removed, R#18).
+// Layout P ("packed", VBDR-gsmall semantics): SetDR on the packed DRV during
+//   the scan (Alg.9) as an atomicAnd on the containing word.
+// Both: DRV = W planes of n_phys u32 words, F = 32/zb DRs per word; rank rho
+//   lives in word (rho-1)/F, field (rho-1)%F.
+#include "vbdr_dev.cuh"
+
+using namespace vbdr_dev;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+  return __ldcg(p);  // L2 (skip L1: other SMs update it)
+}
+
+// ------------------------------------------------------------------ scan
+// One pair: Alg.4 lines 180-184 then the layout's record.
+template <bool FAST, int ZB, int MODE>
+__device__ __forceinline__ void record(uint32_t aip, uint32_t bip, const DevParams &p,
+                                       uint32_t tickbits) {
+  uint32_t pidx, rho;
+  pair_index(aip, bip, p, pidx, rho);
+  if constexpr (FAST) {
+    // nowLBP1 <- max(nowLBP1, LBP1(bip'))
+    const uint32_t val = tickbits | rho;
+    uint32_t *a = p.sr + pidx;
+    if constexpr (MODE == 2) {
+      if (ld_relaxed(a) >= val) return;  // stored value dominates: max is a no-op
+    }
+    atomicMax(a, val);
+  } else {
+    // SetDR(DRV[LBP1(bip')]) = clear one zb-bit field
+    using S = Swar<ZB>;
+    const uint32_t r = rho - 1u;
+    const uint32_t w = r / (uint32_t)S::F;
+    const uint32_t f = r - w * (uint32_t)S::F;
+    const uint32_t fm = S::FM << (ZB * f);
+    uint32_t *a = p.drv + (uint64_t)w * p.n_phys + pidx;
+    if constexpr (MODE == 2) {
+      if ((ld_relaxed(a) & fm) == 0u) return;  // already zero
+    }
+    atomicAnd(a, ~fm);
+  }
+}
+
+// Grid-stride over pairs, two pairs per 16-byte load, UNROLL loads in flight.
+template <bool FAST, int ZB, int MODE>
+__global__ void __launch_bounds__(kThreads)
+k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict__ tail,
+       DevParams p) {
+  constexpr int UNROLL = 4;
+  const uint32_t tickbits = p.tick << 5;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  for (; i + (UNROLL - 1) * stride < n2; i += UNROLL * stride) {
+    uint4 v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) v[u] = __ldcs(pairs2 + i + u * stride);  // streamed once
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      record<FAST, ZB, MODE>(v[u].x, v[u].y, p, tickbits);
+      record<FAST, ZB, MODE>(v[u].z, v[u].w, p, tickbits);
+    }
+  }
+  for (; i < n2; i += stride) {
+    const uint4 v = __ldcs(pairs2 + i);
+    record<FAST, ZB, MODE>(v.x, v.y, p, tickbits);
+    record<FAST, ZB, MODE>(v.z, v.w, p, tickbits);
+  }
+  if (tail != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+    record<FAST, ZB, MODE>(tail[0], tail[1], p, tickbits);
+}
+
+// ------------------------------------------------------------------ slide
+// One thread = 4 consecutive BDRs (16-byte loads of every plane).
+//   FAST:   age all DRs (Alg.1), SetDR(DRV[nowLBP1]) if sr is from
+//           this tick (Alg.1, R#9), M = GetLBP1BDR (Alg.2).
+//   PACKED: M = GetLBP1BDR of the ages at this boundary (Alg.2), then age all
+//           DRs for the next slice (Alg.8 hoisted from the next slice open).
+// Writes regmax[j] = M and accumulates S_tot = sum 2^(L-M), V_tot = #{M=0}.
+template <bool FAST, int ZB>
+__global__ void __launch_bounds__(kThreads)
+k_slide(DevParams p, uint32_t addk, uint32_t slot) {
+  using S = Swar<ZB>;
+  constexpr int WM = WMax<ZB>::value;
+  const uint64_t n4 = p.n_phys >> 2;
+  const uint4 *sr4 = reinterpret_cast<const uint4 *>(p.sr);
+  uint4 *drv4 = reinterpret_cast<uint4 *>(p.drv);
+  uint32_t *reg4 = reinterpret_cast<uint32_t *>(p.regmax);
+  unsigned long long s_acc = 0;
+  uint32_t v_acc = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t q = (uint64_t)blockIdx.x * kThreads + threadIdx.x; q < n4; q += stride) {
+    uint32_t hit[4] = {0u, 0u, 0u, 0u};  // 1 + rank-1 of this slice's max rank, or 0
+    if constexpr (FAST) {
+      const uint4 s = __ldcs(sr4 + q);
+      const uint32_t sv[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) hit[c] = ((sv[c] >> 5) == p.tick) ? (sv[c] & 31u) : 0u;
+    }
+    uint4 x[WM];
+#pragma unroll
+    for (int w = 0; w < WM; ++w)
+      if (w < (int)p.W) x[w] = drv4[(uint64_t)w * n4 + q];
+    uint32_t best[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int w = WM - 1; w >= 0; --w) {
+      if (w >= (int)p.W) continue;
+      uint32_t xv[4] = {x[w].x, x[w].y, x[w].z, x[w].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t a;
+        if constexpr (FAST) {
+          uint32_t y = S::age(xv[c]);
+          if (hit[c] != 0u) {
+            const uint32_t r = hit[c] - 1u;
+            const uint32_t ws = r / (uint32_t)S::F;
+            if (ws == (uint32_t)w) y &= ~(S::FM << (ZB * (r - ws * (uint32_t)S::F)));
+          }
+          xv[c] = y;
+          a = S::active(y, addk);
+        } else {
+          a = S::active(xv[c], addk);
+          xv[c] = S::age(xv[c]);
+        }
+        if (best[c] == 0u && a != 0u) best[c] = (uint32_t)w * S::F + S::top_field(a) + 1u;
+      }
+      drv4[(uint64_t)w * n4 + q] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
+    }
+    reg4[q] = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      s_acc += 1ull << (p.L - best[c]);
+      v_acc += best[c] == 0u;
+    }
+  }
+  // block reduction, one atomic per block (integers: order-independent)
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    s_acc += __shfl_xor_sync(0xffffffffu, s_acc, off);
+    v_acc += __shfl_xor_sync(0xffffffffu, v_acc, off);
+  }
+  __shared__ unsigned long long ss[kThreads / 32];
+  __shared__ uint32_t sv[kThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    ss[warp] = s_acc;
+    sv[warp] = v_acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long st = 0, vt = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      st += ss[w];
+      vt += sv[w];
+    }
+    atomicAdd(p.acc + 2 * slot, st);
+    atomicAdd(p.acc + 2 * slot + 1, vt);
+    if (blockIdx.x == 0) {  // the other parity's slot is next slide's accumulator
+      p.acc[2 * (slot ^ 1u)] = 0ull;
+      p.acc[2 * (slot ^ 1u) + 1] = 0ull;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ init
+// InitDR on every DR, stamps and registers 0.  Accumulator slot
+// 0 describes the empty window (all M = 0) so estimates before the first
+// slide are 0; slot 1 is the first slide's accumulator.
+template <int ZB>
+__global__ void __launch_bounds__(kThreads) k_init(DevParams p, bool fast) {
+  using S = Swar<ZB>;
+  const uint64_t n4 = p.n_phys >> 2;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  uint4 *drv4 = reinterpret_cast<uint4 *>(p.drv);
+  for (uint64_t q = (uint64_t)blockIdx.x * kThreads + threadIdx.x; q < n4; q += stride) {
+    for (uint32_t w = 0; w < p.W; ++w) drv4[(uint64_t)w * n4 + q] = make_uint4(S::INIT, S::INIT, S::INIT, S::INIT);
+    if (fast) reinterpret_cast<uint4 *>(p.sr)[q] = make_uint4(0u, 0u, 0u, 0u);
+    reinterpret_cast<uint32_t *>(p.regmax)[q] = 0u;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.acc[0] = (unsigned long long)p.n_phys << p.L;
+    p.acc[1] = p.n_phys;
+    p.acc[2] = 0ull;
+    p.acc[3] = 0ull;
+  }
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+uint32_t grid_for(uint64_t work, int blocks_per_sm) {
+  const uint64_t need = (work + kThreads - 1) / kThreads;
+  const uint64_t cap = (uint64_t)sm_count() * blocks_per_sm;
+  uint64_t g = need < cap ? need : cap;
+  return (uint32_t)(g ? g : 1);
+}
+
+template <template <int> class Fn, typename... Args>
+cudaError_t dispatch_zb(uint32_t zb, Args &&...args) {
+  switch (zb) {
+    case 1: return Fn<1>::run(args...);
+    case 2: return Fn<2>::run(args...);
+    case 3: return Fn<3>::run(args...);
+    case 4: return Fn<4>::run(args...);
+    case 5: return Fn<5>::run(args...);
+    case 6: return Fn<6>::run(args...);
+    case 7: return Fn<7>::run(args...);
+    case 8: return Fn<8>::run(args...);
+    case 9: return Fn<9>::run(args...);
+    case 10: return Fn<10>::run(args...);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int ZB>
+struct InitFn {
+  static cudaError_t run(const DevParams &p, bool fast, cudaStream_t s) {
+    k_init<ZB><<<grid_for(p.n_phys >> 2, 8), kThreads, 0, s>>>(p, fast);
+    return cudaGetLastError();
+  }
+};
+
+template <int ZB>
+struct SlideFn {
+  static cudaError_t run(const DevParams &p, bool fast, cudaStream_t s) {
+    // (2^zb - k) at every even field's LSB (Swar::active)
+    uint32_t addk = 0;
+    for (uint32_t f = 0; f < Swar<ZB>::F; f += 2) addk |= ((1u << ZB) - p.k) << (ZB * f);
+    const uint32_t slot = p.tick & 1u;
+    const uint32_t grid = grid_for(p.n_phys >> 2, 8);
+    if (fast)
+      k_slide<true, ZB><<<grid, kThreads, 0, s>>>(p, addk, slot);
+    else
+      k_slide<false, ZB><<<grid, kThreads, 0, s>>>(p, addk, slot);
+    return cudaGetLastError();
+  }
+};
+
+template <int ZB>
+struct ScanPackedFn {
+  static cudaError_t run(const DevParams &p, int mode, const uint4 *pairs2, uint64_t n2,
+                         const uint32_t *tail, uint32_t grid, cudaStream_t s) {
+    if (mode == 2)
+      k_scan<false, ZB, 2><<<grid, kThreads, 0, s>>>(pairs2, n2, tail, p);
+    else
+      k_scan<false, ZB, 1><<<grid, kThreads, 0, s>>>(pairs2, n2, tail, p);
+    return cudaGetLastError();
+  }
+};
+
+}  // namespace
+
+namespace vbdr_launch {
+
+cudaError_t init(const DevParams &p, bool fast, cudaStream_t s) {
+  return dispatch_zb<InitFn>(p.zb, p, fast, s);
+}
+
+cudaError_t slide(const DevParams &p, bool fast, cudaStream_t s) {
+  return dispatch_zb<SlideFn>(p.zb, p, fast, s);
+}
+
+cudaError_t scan(const DevParams &p, bool fast, int mode, const uint32_t *pairs, uint64_t n,
+                 cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const uint64_t n2 = n >> 1;
+  const uint32_t *tail = (n & 1u) ? pairs + 2 * (n - 1) : nullptr;
+  const uint4 *pairs2 = reinterpret_cast<const uint4 *>(pairs);
+  const uint32_t grid = grid_for(n2 ? n2 : 1, 8);
+  if (fast) {
+    if (mode == 2)
+      k_scan<true, 1, 2><<<grid, kThreads, 0, s>>>(pairs2, n2, tail, p);
+    else
+      k_scan<true, 1, 1><<<grid, kThreads, 0, s>>>(pairs2, n2, tail, p);
+    return cudaGetLastError();
+  }
+  return dispatch_zb<ScanPackedFn>(p.zb, p, mode, pairs2, n2, tail, grid, s);
+}
+
+}  // namespace vbdr_launch

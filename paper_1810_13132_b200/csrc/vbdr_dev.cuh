@@ -1,0 +1,121 @@
+// vbdr_dev.cuh -- device-side building blocks of the VBDR hot path (sm_100a).
+//
+// Shared by the kernels of libvbdr.so only (never by oracle/).  Citations:
+// PAPER.md:N = line of the paper text; R#n = DESIGN.md section 3 reading.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vbdr_dev {
+
+// Parameters every kernel receives by value.
+struct DevParams {
+  uint32_t *sr;              // u32[n_phys] stamp words (layout F)
+  uint32_t *drv;             // u32[W][n_phys] packed DRV, plane-major
+  uint8_t *regmax;           // u8[n_phys] register values M[j]
+  unsigned long long *acc;   // u64[4]: (S_tot, V_tot) per tick parity
+  uint64_t n_phys;
+  uint32_t mask;             // n_phys - 1 (n_phys <= 2^32)
+  uint32_t b, L, k, zb, F, W;
+  uint32_t A0, A1;
+  uint32_t tick;             // T of the open slice
+};
+
+// H(x, 2^32, A) = fmix32(x ^ A) (R#6: MurmurHash3 finaliser).
+__device__ __forceinline__ uint32_t fmix32(uint32_t t) {
+  t ^= t >> 16;
+  t *= 0x85EBCA6Bu;
+  t ^= t >> 13;
+  t *= 0xC2B2AE35u;
+  t ^= t >> 16;
+  return t;
+}
+
+// Alg.4 lines 180-184 for one pair, in registers:
+//   bip' = H(bip, 2^32, A1); vidx = LB(bip', b); w = bip' << b;
+//   rho  = LBP1(w) = min(clz(w) + 1, L)          (R#4, R#5)
+//   pidx = getPhyIdx(aip, vidx, A0) = H(aip, z, H(vidx, 2^32, A0))  (Alg.3)
+__device__ __forceinline__ void pair_index(uint32_t aip, uint32_t bip, const DevParams &p,
+                                           uint32_t &pidx, uint32_t &rho) {
+  const uint32_t bp = fmix32(bip ^ p.A1);
+  const uint32_t vidx = bp >> (32u - p.b);
+  const uint32_t w = bp << p.b;
+  rho = min((uint32_t)__clz(w) + 1u, p.L);
+  const uint32_t s1 = fmix32(vidx ^ p.A0);
+  pidx = fmix32(aip ^ s1) & p.mask;
+}
+
+// SWAR over one 32-bit word of F = 32/ZB packed DRs (field f = bits
+// [ZB f, ZB f + ZB)).  Unused high bits are kept zero.
+template <int ZB>
+struct Swar {
+  static constexpr int F = 32 / ZB;
+  static constexpr uint32_t FM = (1u << ZB) - 1u;  // one field, all ones = sentinel S
+  static constexpr uint32_t lsb_of(int parity) {   // parity: 0 even, 1 odd, 2 all
+    uint32_t m = 0;
+    for (int f = 0; f < F; ++f)
+      if (parity == 2 || (f & 1) == parity) m |= 1u << (ZB * f);
+    return m;
+  }
+  static constexpr uint32_t LSB = lsb_of(2);
+  static constexpr uint32_t LSB_EVEN = lsb_of(0);
+  static constexpr uint32_t CARRY = LSB_EVEN << ZB;  // carry-out bit of each even slot
+  static constexpr uint32_t EVEN = LSB_EVEN * FM;  // fields 0, 2, 4, ...
+  static constexpr uint32_t INIT = LSB * FM;        // InitDR on every field
+
+  // SlideDR on every field (R#1: saturating at S = 2^ZB - 1).
+  __device__ static __forceinline__ uint32_t age(uint32_t x) {
+    uint32_t t = x;
+#pragma unroll
+    for (int i = 1; i < ZB; ++i) t &= x >> i;  // bit ZB f = AND of field f's bits
+    return x + (LSB & ~t);                     // +1 where the field is not S
+  }
+
+  // IsActiveDR (dr < k) on every field: returns bit ZB f set iff
+  // field f < k.  addk = (2^ZB - k) at every even field's LSB; a field >= k
+  // carries into the (zeroed) neighbour above it.
+  __device__ static __forceinline__ uint32_t active(uint32_t x, uint32_t addk) {
+    const uint32_t ce = ((x & EVEN) + addk) & CARRY;          // even field f -> bit ZB(f+1)
+    const uint32_t co = (((x >> ZB) & EVEN) + addk) & CARRY;  // odd field f  -> bit ZB f
+    const uint32_t inactive = (ce >> ZB) | co;  // bit ZB f; a phantom field F is masked off
+    return ~inactive & LSB;
+  }
+
+  // Highest active field of a non-zero mask from active().
+  __device__ static __forceinline__ uint32_t top_field(uint32_t a) {
+    return (31u - (uint32_t)__clz(a)) / (uint32_t)ZB;
+  }
+};
+
+// Max useful words per BDR for a field width (L <= 31 ranks).
+template <int ZB>
+struct WMax {
+  static constexpr int value = (31 + Swar<ZB>::F - 1) / Swar<ZB>::F;
+};
+
+}  // namespace vbdr_dev
+
+// Launchers implemented in the .cu files (host side, return cudaError_t).
+namespace vbdr_launch {
+using vbdr_dev::DevParams;
+cudaError_t init(const DevParams &p, bool fast, cudaStream_t s);
+cudaError_t scan(const DevParams &p, bool fast, int mode, const uint32_t *pairs, uint64_t n,
+                 cudaStream_t s);
+cudaError_t slide(const DevParams &p, bool fast, cudaStream_t s);
+
+struct EstParams {
+  const uint8_t *regmax;
+  const unsigned long long *acc;  // (S_tot, V_tot) of the closed tick
+  uint32_t mask, A0, L, g;
+  double inv2L;       // 2^-L
+  double agg;         // alpha_g * g * g
+  double lc_g;        // 2.5 * g
+  double azz;         // alpha_z * z * z
+  double lc_z;        // 2.5 * z
+  double z;           // n_phys as double
+  double C;           // z g / (z - g)
+};
+cudaError_t estimate(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
+                     unsigned long long *outS, uint32_t *outV, cudaStream_t s);
+}  // namespace vbdr_launch

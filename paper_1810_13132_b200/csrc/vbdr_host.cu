@@ -1,0 +1,440 @@
+// vbdr_host.cu -- the C ABI of libvbdr.so (declared in include/vbdr.h):
+// configuration validation, state-layout planning, launches, host-buffer
+// pipelines and parity exports.  No compute happens on the host: every step of
+// the path runs in the kernels of k_scan_slide.cu and k_estimate.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/vbdr.h"
+#include "vbdr_dev.cuh"
+
+using vbdr_dev::DevParams;
+
+struct vbdr {
+  vbdr_config cfg{};
+  vbdr_info_t info{};
+  DevParams p{};
+  bool fast = true;
+  double alpha_g = 0, alpha_z = 0;
+  std::string err;
+  // host-buffer pipeline resources (created on first use)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+  cudaEvent_t ev_scanned[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+constexpr uint32_t kTickLimit = 1u << 26;  // sr = (T << 5) | rho < 2^31: also a valid int32 for MAX merges
+
+uint64_t align256(uint64_t x) { return (x + 255u) & ~uint64_t(255); }
+
+bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+uint32_t log2u(uint64_t x) {
+  uint32_t r = 0;
+  while ((1ull << r) < x) ++r;
+  return r;
+}
+
+// HyperLogLog alpha_s (R#16), same double operations as the oracle.
+double alpha_of(uint64_t s) {
+  if (s == 16) return 0.673;
+  if (s == 32) return 0.697;
+  if (s == 64) return 0.709;
+  return 0.7213 / (1.0 + 1.079 / (double)s);
+}
+
+struct Plan {
+  uint32_t b, L, zb, F, W;
+  uint64_t off_acc, off_sr, off_drv, off_regmax, bytes;
+};
+
+// Validate a config and lay out the state buffer.  Returns an error text or
+// empty on success.
+std::string plan(const vbdr_config *c, vbdr_config *norm, Plan *pl) {
+  if (!c) return "null config";
+  vbdr_config n = *c;
+  if (n.seed_a0 == 0 && n.seed_a1 == 0) {  // R#7 defaults
+    n.seed_a0 = 0x5EED0001u;
+    n.seed_a1 = 0x5EED0002u;
+  }
+  if (n.layout > 1) return "layout must be 0 (fast) or 1 (packed)";
+  if (n.scan_mode > 3) return "scan_mode must be 0..3";
+  if (n.m < 2 || !is_pow2(n.m)) return "m must be a power of two >= 2";
+  if (n.k < 1) return "k must be >= 1";
+  if (n.n_phys < 4 || !is_pow2(n.n_phys) || n.n_phys > (1ull << 32))
+    return "n_phys must be a power of two in [4, 2^32]";
+  if (2ull * n.m > n.n_phys) return "2*m must be <= n_phys (vHLL denominator, R#15)";
+  if (n.n_phys / n.m > (1ull << 21)) return "n_phys/m must be <= 2^21 (exact fp64 pool sums)";
+  const uint32_t b = log2u(n.m);
+  if (b > 31) return "m too large";
+  const uint32_t L = n.rank_cap ? n.rank_cap : 32u - b;
+  if (L < 1 || L > 32u - b) return "rank_cap must be in [1, 32 - log2(m)]";
+  uint32_t zb = n.zbits;
+  const bool packed = n.layout == VBDR_LAYOUT_PACKED;
+  if (zb == 0) {
+    zb = log2u((uint64_t)n.k + 1);
+    if (zb == 0) zb = 1;
+    if (packed && ((1ull << zb) - 2) < n.k) zb += 1;  // R#2: S - 1 >= k for layout P
+  }
+  if (zb < 1 || zb > 10) return "zbits must be in [1, 10]";
+  if (((1ull << zb) - 1) < n.k) return "2^zbits - 1 must be >= k (PAPER.md:92)";
+  if (packed && ((1ull << zb) - 2) < n.k)
+    return "layout packed needs 2^zbits - 2 >= k (canonical export, R#2)";
+  n.zbits = zb;
+  n.rank_cap = L;
+  const uint32_t F = 32u / zb;
+  const uint32_t W = (L + F - 1) / F;
+  uint64_t off = 0;
+  pl->off_acc = off;
+  off = align256(off + 4 * sizeof(uint64_t));
+  pl->off_sr = off;
+  if (!packed) off = align256(off + 4ull * n.n_phys);
+  pl->off_drv = off;
+  off = align256(off + 4ull * W * n.n_phys);
+  pl->off_regmax = off;
+  off = align256(off + n.n_phys);
+  pl->bytes = off;
+  pl->b = b;
+  pl->L = L;
+  pl->zb = zb;
+  pl->F = F;
+  pl->W = W;
+  *norm = n;
+  return {};
+}
+
+vbdr_status fail(vbdr *h, vbdr_status s, const std::string &msg) {
+  if (h) h->err = msg;
+  return s;
+}
+
+vbdr_status cuda_fail(vbdr *h, cudaError_t e, const char *where) {
+  return fail(h, VBDR_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Sticky or pending asynchronous errors surface on the next call.
+vbdr_status check_async(vbdr *h, const char *where) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(h, e, where);
+  return VBDR_OK;
+}
+
+cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+vbdr_launch::EstParams est_params(const vbdr *h) {
+  vbdr_launch::EstParams e{};
+  const uint32_t closed = h->p.tick - 1u;  // tick of the last boundary (0 = none)
+  e.regmax = h->p.regmax;
+  e.acc = h->p.acc + 2 * (closed & 1u);
+  e.mask = h->p.mask;
+  e.A0 = h->p.A0;
+  e.L = h->p.L;
+  e.g = h->cfg.m;
+  e.inv2L = std::ldexp(1.0, -(int)h->p.L);
+  const double g = (double)h->cfg.m, z = (double)h->cfg.n_phys;
+  e.agg = h->alpha_g * g * g;  // exact: g is a power of two
+  e.lc_g = 2.5 * g;
+  e.azz = h->alpha_z * z * z;
+  e.lc_z = 2.5 * z;
+  e.z = z;
+  e.C = ((double)h->cfg.n_phys * (double)h->cfg.m) / (double)(h->cfg.n_phys - h->cfg.m);
+  return e;
+}
+
+vbdr_status ensure_pipeline(vbdr *h) {
+  if (h->copy_stream) return VBDR_OK;
+  cudaError_t e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&h->ev_copied[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_scanned[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) return cuda_fail(h, e, "pipeline resources");
+  return VBDR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *vbdr_status_string(vbdr_status s) {
+  switch (s) {
+    case VBDR_OK: return "ok";
+    case VBDR_EINVAL: return "invalid argument";
+    case VBDR_ERANGE: return "out of range";
+    case VBDR_ESTATE: return "invalid state";
+    case VBDR_ENOMEM: return "out of memory";
+    case VBDR_ECUDA: return "cuda error";
+  }
+  return "unknown";
+}
+
+const char *vbdr_last_error(const vbdr_t *h) { return h ? h->err.c_str() : "null handle"; }
+
+vbdr_status vbdr_state_bytes(const vbdr_config *cfg, uint64_t *bytes) {
+  if (!bytes) return VBDR_EINVAL;
+  vbdr_config n;
+  Plan pl;
+  if (!plan(cfg, &n, &pl).empty()) return VBDR_EINVAL;
+  *bytes = pl.bytes;
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, void *stream,
+                        vbdr_t **out) {
+  if (!out) return VBDR_EINVAL;
+  *out = nullptr;
+  vbdr *h = new (std::nothrow) vbdr();
+  if (!h) return VBDR_ENOMEM;
+  Plan pl;
+  std::string e = plan(cfg, &h->cfg, &pl);
+  if (!e.empty() || !d_state || (reinterpret_cast<uintptr_t>(d_state) & 255u)) {
+    delete h;
+    return VBDR_EINVAL;
+  }
+  if (bytes < pl.bytes) {
+    delete h;
+    return VBDR_ENOMEM;
+  }
+  cudaGetLastError();  // do not inherit someone else's error
+  h->fast = h->cfg.layout == VBDR_LAYOUT_FAST;
+  uint8_t *base = static_cast<uint8_t *>(d_state);
+  DevParams &p = h->p;
+  p.acc = reinterpret_cast<unsigned long long *>(base + pl.off_acc);
+  p.sr = h->fast ? reinterpret_cast<uint32_t *>(base + pl.off_sr) : nullptr;
+  p.drv = reinterpret_cast<uint32_t *>(base + pl.off_drv);
+  p.regmax = base + pl.off_regmax;
+  p.n_phys = h->cfg.n_phys;
+  p.mask = (uint32_t)(h->cfg.n_phys - 1);
+  p.b = pl.b;
+  p.L = pl.L;
+  p.k = h->cfg.k;
+  p.zb = pl.zb;
+  p.F = pl.F;
+  p.W = pl.W;
+  p.A0 = h->cfg.seed_a0;
+  p.A1 = h->cfg.seed_a1;
+  p.tick = 1;  // slice t = 0 is open, T = t + 1
+  h->alpha_g = alpha_of(h->cfg.m);
+  h->alpha_z = alpha_of(h->cfg.n_phys);
+  vbdr_info_t &in = h->info;
+  in.b = pl.b;
+  in.L = pl.L;
+  in.zbits = pl.zb;
+  in.fields = pl.F;
+  in.words = pl.W;
+  in.n_phys = h->cfg.n_phys;
+  in.off_acc = pl.off_acc;
+  in.off_sr = h->fast ? pl.off_sr : ~0ull;
+  in.off_drv = pl.off_drv;
+  in.off_regmax = pl.off_regmax;
+  in.state_bytes = pl.bytes;
+  const cudaError_t ce = vbdr_launch::init(p, h->fast, S(stream));
+  if (ce != cudaSuccess) {
+    delete h;
+    return VBDR_ECUDA;
+  }
+  in.launches = 1;
+  *out = h;
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_destroy(vbdr_t *h) {
+  if (!h) return VBDR_EINVAL;
+  if (h->copy_stream) {
+    cudaStreamSynchronize(h->copy_stream);
+    cudaStreamDestroy(h->copy_stream);
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
+    if (h->ev_scanned[i]) cudaEventDestroy(h->ev_scanned[i]);
+  }
+  delete h;
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_info(const vbdr_t *h, vbdr_info_t *info) {
+  if (!h || !info) return VBDR_EINVAL;
+  *info = h->info;
+  info->tick = h->p.tick;
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_scan_slice(vbdr_t *h, const uint32_t *d_pairs, uint64_t n_pairs, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (n_pairs == 0) return VBDR_OK;  // an empty batch still leaves the slice open
+  if (!d_pairs || (reinterpret_cast<uintptr_t>(d_pairs) & 15u))
+    return fail(h, VBDR_EINVAL, "d_pairs must be a 16-byte aligned device pointer");
+  if (vbdr_status s = check_async(h, "before scan")) return s;
+  const int mode = h->cfg.scan_mode == 0 ? 1 : (int)h->cfg.scan_mode;
+  const cudaError_t e = vbdr_launch::scan(h->p, h->fast, mode == 3 ? 1 : mode, d_pairs, n_pairs,
+                                          S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "scan launch");
+  h->info.launches += 1;
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_slide(vbdr_t *h, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (vbdr_status s = check_async(h, "before slide")) return s;
+  const cudaError_t e = vbdr_launch::slide(h->p, h->fast, S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "slide launch");
+  h->info.launches += 1;
+  h->info.slices_closed += 1;
+  h->p.tick += 1;
+  if (h->p.tick >= kTickLimit) {
+    // Every stamp is stale after a slide; restart the tick at 2 (same parity
+    // as kTickLimit, so the accumulator slots keep alternating).
+    if (h->fast) {
+      const cudaError_t m = cudaMemsetAsync(h->p.sr, 0, 4ull * h->p.n_phys, S(stream));
+      if (m != cudaSuccess) return cuda_fail(h, m, "tick wrap");
+    }
+    h->p.tick = 2;
+  }
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_estimate(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, double *d_out,
+                          void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (n_hosts == 0) return VBDR_OK;
+  if (!d_hosts || !d_out) return fail(h, VBDR_EINVAL, "null d_hosts/d_out");
+  if (vbdr_status s = check_async(h, "before estimate")) return s;
+  const cudaError_t e =
+      vbdr_launch::estimate(est_params(h), d_hosts, n_hosts, d_out, nullptr, nullptr, S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "estimate launch");
+  h->info.launches += 1;
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_host_sums(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, uint64_t *d_S,
+                           uint32_t *d_V, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (n_hosts == 0) return VBDR_OK;
+  if (!d_hosts || !d_S || !d_V) return fail(h, VBDR_EINVAL, "null pointer");
+  if (vbdr_status s = check_async(h, "before host_sums")) return s;
+  const cudaError_t e = vbdr_launch::estimate(est_params(h), d_hosts, n_hosts, nullptr,
+                                              reinterpret_cast<unsigned long long *>(d_S), d_V,
+                                              S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "host_sums launch");
+  h->info.launches += 1;
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_scan_slice_host(vbdr_t *h, const uint32_t *h_pairs, uint64_t n_pairs,
+                                 uint32_t *d_stage, uint64_t stage_pairs, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (n_pairs == 0) return VBDR_OK;
+  if (!h_pairs || !d_stage || stage_pairs < 16 ||
+      (reinterpret_cast<uintptr_t>(d_stage) & 15u))
+    return fail(h, VBDR_EINVAL, "bad host pairs / staging buffer");
+  if (vbdr_status s = ensure_pipeline(h)) return s;
+  if (vbdr_status s = check_async(h, "before scan_host")) return s;
+  cudaStream_t cs = S(stream);
+  // two halves of the staging buffer, each a multiple of 2 pairs (16 B)
+  const uint64_t half = (stage_pairs / 2) & ~uint64_t(1);
+  // the copy stream must not overtake work already queued on `stream`
+  cudaError_t e = cudaEventRecord(h->ev_scanned[0], cs);
+  if (e == cudaSuccess) e = cudaEventRecord(h->ev_scanned[1], cs);
+  uint64_t done = 0;
+  for (uint64_t c = 0; done < n_pairs && e == cudaSuccess; ++c) {
+    const int slot = (int)(c & 1u);
+    const uint64_t cnt = (n_pairs - done) < half ? (n_pairs - done) : half;
+    uint32_t *dst = d_stage + 2 * half * (uint64_t)slot;
+    e = cudaStreamWaitEvent(h->copy_stream, h->ev_scanned[slot], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(dst, h_pairs + 2 * done, 8ull * cnt, cudaMemcpyHostToDevice,
+                          h->copy_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_copied[slot], h->copy_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, h->ev_copied[slot], 0);
+    if (e == cudaSuccess) {
+      const int mode = h->cfg.scan_mode == 0 ? 1 : (int)h->cfg.scan_mode;
+      e = vbdr_launch::scan(h->p, h->fast, mode == 3 ? 1 : mode, dst, cnt, cs);
+      h->info.launches += 1;
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_scanned[slot], cs);
+    done += cnt;
+  }
+  if (e != cudaSuccess) return cuda_fail(h, e, "scan_host");
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_estimate_host(vbdr_t *h, const uint32_t *h_hosts, uint64_t n_hosts,
+                               uint32_t *d_hosts_stage, double *d_out_stage, double *h_out,
+                               void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (n_hosts == 0) return VBDR_OK;
+  if (!h_hosts || !d_hosts_stage || !d_out_stage || !h_out)
+    return fail(h, VBDR_EINVAL, "null pointer");
+  if (vbdr_status s = check_async(h, "before estimate_host")) return s;
+  cudaStream_t cs = S(stream);
+  cudaError_t e =
+      cudaMemcpyAsync(d_hosts_stage, h_hosts, 4ull * n_hosts, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess)
+    e = vbdr_launch::estimate(est_params(h), d_hosts_stage, n_hosts, d_out_stage, nullptr,
+                              nullptr, cs);
+  if (e == cudaSuccess) {
+    h->info.launches += 1;
+    e = cudaMemcpyAsync(h_out, d_out_stage, 8ull * n_hosts, cudaMemcpyDeviceToHost, cs);
+  }
+  if (e != cudaSuccess) return cuda_fail(h, e, "estimate_host");
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_export_ages(vbdr_t *h, uint16_t *h_ages, int mode, void *stream) {
+  if (!h || !h_ages || (mode != 0 && mode != 1)) return VBDR_EINVAL;
+  const uint64_t n = h->p.n_phys;
+  const uint32_t W = h->p.W, F = h->p.F, zb = h->p.zb, L = h->p.L, k = h->p.k;
+  std::vector<uint32_t> words;
+  try {
+    words.resize((size_t)(W * n));
+  } catch (...) {
+    return fail(h, VBDR_ENOMEM, "host buffer");
+  }
+  cudaStream_t cs = S(stream);
+  cudaError_t e = cudaMemcpyAsync(words.data(), h->p.drv, 4ull * W * n, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return cuda_fail(h, e, "export_ages");
+  const uint32_t fm = (1u << zb) - 1u, sent = fm;
+  for (uint64_t j = 0; j < n; ++j) {
+    for (uint32_t r = 1; r <= L; ++r) {
+      const uint32_t w = (r - 1) / F, f = (r - 1) % F;
+      uint32_t v = (words[(size_t)(w * n + j)] >> (zb * f)) & fm;
+      if (mode == 1) {
+        if (!h->fast) v = (v == sent) ? k : (v ? v - 1u : 0u);  // undo the hoisted Alg.8 ageing
+        if (v > k) v = k;
+      }
+      h_ages[j * L + (r - 1)] = (uint16_t)v;
+    }
+  }
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_export_regmax(vbdr_t *h, uint8_t *h_regmax, void *stream) {
+  if (!h || !h_regmax) return VBDR_EINVAL;
+  cudaStream_t cs = S(stream);
+  cudaError_t e = cudaMemcpyAsync(h_regmax, h->p.regmax, h->p.n_phys, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return cuda_fail(h, e, "export_regmax");
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_export_pool_sums(vbdr_t *h, uint64_t *h_S_tot, uint64_t *h_V_tot, void *stream) {
+  if (!h || !h_S_tot || !h_V_tot) return VBDR_EINVAL;
+  const uint32_t closed = h->p.tick - 1u;
+  unsigned long long v[2];
+  cudaStream_t cs = S(stream);
+  cudaError_t e = cudaMemcpyAsync(v, h->p.acc + 2 * (closed & 1u), sizeof v,
+                                  cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return cuda_fail(h, e, "export_pool_sums");
+  *h_S_tot = v[0];
+  *h_V_tot = v[1];
+  return VBDR_OK;
+}
+
+}  // extern "C"

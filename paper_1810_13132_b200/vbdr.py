@@ -1,0 +1,259 @@
+"""Thin Python binding of libvbdr.so (include/vbdr.h) -- argument marshalling only.
+
+PyTorch provides device memory, streams and process groups; every step of the
+VBDR path runs in the library's CUDA kernels.  There is no CPU fallback: if the
+native library is missing or CUDA is unavailable, construction raises.
+
+Names follow the C ABI: ``vbdr_create`` -> :class:`VBDR`, ``vbdr_scan_slice``
+-> :meth:`VBDR.scan_slice`, ``vbdr_slide`` -> :meth:`VBDR.slide`,
+``vbdr_estimate`` -> :meth:`VBDR.estimate`, ``vbdr_destroy`` -> :meth:`VBDR.close`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libvbdr.so")
+
+LAYOUT_FAST, LAYOUT_PACKED = 0, 1
+LAYOUTS = {"fast": LAYOUT_FAST, "packed": LAYOUT_PACKED}
+
+STATUS = {0: "ok", -1: "EINVAL", -2: "ERANGE", -3: "ESTATE", -4: "ENOMEM", -5: "ECUDA"}
+
+
+class vbdr_config(C.Structure):
+    _fields_ = [("m", C.c_uint32), ("k", C.c_uint32), ("n_phys", C.c_uint64),
+                ("seed_a0", C.c_uint32), ("seed_a1", C.c_uint32), ("zbits", C.c_uint32),
+                ("rank_cap", C.c_uint32), ("layout", C.c_uint32), ("scan_mode", C.c_uint32)]
+
+
+class vbdr_info_t(C.Structure):
+    _fields_ = [("b", C.c_uint32), ("L", C.c_uint32), ("zbits", C.c_uint32),
+                ("fields", C.c_uint32), ("words", C.c_uint32), ("tick", C.c_uint32),
+                ("n_phys", C.c_uint64), ("slices_closed", C.c_uint64), ("off_acc", C.c_uint64),
+                ("off_sr", C.c_uint64), ("off_drv", C.c_uint64), ("off_regmax", C.c_uint64),
+                ("state_bytes", C.c_uint64), ("launches", C.c_uint64)]
+
+
+# Every symbol include/vbdr.h declares (tests check the library exports them).
+SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice", "vbdr_slide",
+           "vbdr_estimate", "vbdr_host_sums", "vbdr_scan_slice_host", "vbdr_estimate_host",
+           "vbdr_info", "vbdr_export_ages", "vbdr_export_regmax", "vbdr_export_pool_sums",
+           "vbdr_last_error", "vbdr_status_string")
+
+_lib = None
+
+
+def lib():
+    """Load libvbdr.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build(); "
+                               "there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        vp, u64, u32 = C.c_void_p, C.c_uint64, C.c_uint32
+        sig = {
+            "vbdr_state_bytes": [C.POINTER(vbdr_config), C.POINTER(u64)],
+            "vbdr_create": [C.POINTER(vbdr_config), vp, u64, vp, C.POINTER(vp)],
+            "vbdr_destroy": [vp],
+            "vbdr_scan_slice": [vp, vp, u64, vp],
+            "vbdr_slide": [vp, vp],
+            "vbdr_estimate": [vp, vp, u64, vp, vp],
+            "vbdr_host_sums": [vp, vp, u64, vp, vp, vp],
+            "vbdr_scan_slice_host": [vp, vp, u64, vp, u64, vp],
+            "vbdr_estimate_host": [vp, vp, u64, vp, vp, vp, vp],
+            "vbdr_info": [vp, C.POINTER(vbdr_info_t)],
+            "vbdr_export_ages": [vp, vp, C.c_int, vp],
+            "vbdr_export_regmax": [vp, vp, vp],
+            "vbdr_export_pool_sums": [vp, C.POINTER(u64), C.POINTER(u64), vp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.vbdr_last_error.argtypes = [vp]
+        L.vbdr_last_error.restype = C.c_char_p
+        L.vbdr_status_string.argtypes = [C.c_int]
+        L.vbdr_status_string.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def make_config(m: int, k: int, n_phys: int, seed_a0: int = 0x5EED0001,
+                seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
+                layout: str | int = "fast", scan_mode: int = 0) -> vbdr_config:
+    lay = LAYOUTS[layout] if isinstance(layout, str) else int(layout)
+    return vbdr_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, lay, scan_mode)
+
+
+def state_bytes(cfg: vbdr_config) -> int:
+    out = C.c_uint64()
+    rc = lib().vbdr_state_bytes(C.byref(cfg), C.byref(out))
+    if rc != 0:
+        raise ValueError(f"vbdr_state_bytes: invalid config ({STATUS.get(rc, rc)})")
+    return out.value
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class VBDR:
+    """One VBDR pool on one GPU (``vbdr_create``).  The state tensor is owned here
+    (PyTorch memory); the library keeps only pointers into it."""
+
+    def __init__(self, m: int, k: int, n_phys: int, *, seed_a0: int = 0x5EED0001,
+                 seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
+                 layout: str = "fast", scan_mode: int = 0, device=None, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("VBDR needs a CUDA device (no CPU fallback)")
+        self.device = torch.device(device if device is not None else "cuda")
+        self.cfg = make_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, layout, scan_mode)
+        nbytes = state_bytes(self.cfg)
+        with torch.cuda.device(self.device):
+            self.state = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            h = C.c_void_p()
+            self._check(lib().vbdr_create(C.byref(self.cfg), C.c_void_p(self.state.data_ptr()),
+                                          nbytes, _stream_ptr(stream), C.byref(h)), "vbdr_create")
+        self._h = h
+        self.m, self.k, self.n_phys = m, k, n_phys
+        self.layout = layout
+
+    # -------------------------------------------------------------- helpers
+    def _check(self, rc: int, what: str):
+        if rc != 0:
+            h = getattr(self, "_h", None)
+            msg = lib().vbdr_last_error(h).decode() if h else ""
+            raise RuntimeError(f"{what} failed: {STATUS.get(rc, rc)} {msg}")
+
+    def close(self):
+        """``vbdr_destroy`` (the state tensor is released by PyTorch)."""
+        if getattr(self, "_h", None):
+            lib().vbdr_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        inf = vbdr_info_t()
+        self._check(lib().vbdr_info(self._h, C.byref(inf)), "vbdr_info")
+        return {name: getattr(inf, name) for name, _ in vbdr_info_t._fields_}
+
+    def sr_view(self):
+        """The stamp words (layout fast) as an int32 tensor view for the
+        multi-GPU max merge: all stamps are < 2^31, so signed MAX is exact."""
+        import torch
+        inf = self.info()
+        if self.layout != "fast":
+            raise RuntimeError("only the fast layout has mergeable stamps")
+        off = inf["off_sr"]
+        return self.state[off:off + 4 * self.n_phys].view(torch.int32)
+
+    # --------------------------------------------------------------- the path
+    def scan_slice(self, pairs, stream=None):
+        """``vbdr_scan_slice``: pairs is a device uint32/int32 tensor of 2*n (aip, bip)."""
+        assert pairs.is_cuda and pairs.is_contiguous() and pairs.element_size() == 4
+        self._check(lib().vbdr_scan_slice(self._h, C.c_void_p(pairs.data_ptr()), pairs.numel() // 2,
+                                          _stream_ptr(stream)), "vbdr_scan_slice")
+
+    def slide(self, stream=None, group=None):
+        """``vbdr_slide``; with a process group of size > 1, first merge the
+        stamp arrays of all ranks by elementwise max (NCCL allreduce MAX)."""
+        if group is not None:
+            merge_stamps(self, group)
+        self._check(lib().vbdr_slide(self._h, _stream_ptr(stream)), "vbdr_slide")
+
+    def estimate(self, hosts, out=None, stream=None):
+        """``vbdr_estimate``: hosts is a device uint32/int32 tensor; returns float64."""
+        import torch
+        assert hosts.is_cuda and hosts.is_contiguous() and hosts.element_size() == 4
+        if out is None:
+            out = torch.empty(hosts.numel(), dtype=torch.float64, device=hosts.device)
+        self._check(lib().vbdr_estimate(self._h, C.c_void_p(hosts.data_ptr()), hosts.numel(),
+                                        C.c_void_p(out.data_ptr()), _stream_ptr(stream)),
+                    "vbdr_estimate")
+        return out
+
+    def host_sums(self, hosts, stream=None):
+        """``vbdr_host_sums``: per host (S, V) of the integer stage."""
+        import torch
+        n = hosts.numel()
+        S = torch.empty(n, dtype=torch.int64, device=hosts.device)
+        V = torch.empty(n, dtype=torch.int32, device=hosts.device)
+        self._check(lib().vbdr_host_sums(self._h, C.c_void_p(hosts.data_ptr()), n,
+                                         C.c_void_p(S.data_ptr()), C.c_void_p(V.data_ptr()),
+                                         _stream_ptr(stream)), "vbdr_host_sums")
+        return S, V
+
+    # ---------------------------------------------------- host-buffer path
+    def scan_slice_host(self, h_pairs, d_stage, stream=None):
+        """``vbdr_scan_slice_host``: h_pairs a (pinned) CPU tensor of 2*n u32."""
+        assert not h_pairs.is_cuda and h_pairs.is_contiguous()
+        self._check(lib().vbdr_scan_slice_host(self._h, C.c_void_p(h_pairs.data_ptr()),
+                                               h_pairs.numel() // 2,
+                                               C.c_void_p(d_stage.data_ptr()),
+                                               d_stage.numel() // 2, _stream_ptr(stream)),
+                    "vbdr_scan_slice_host")
+
+    def estimate_host(self, h_hosts, d_hosts_stage, d_out_stage, h_out, stream=None):
+        """``vbdr_estimate_host``: CPU hosts in, CPU float64 estimates out."""
+        self._check(lib().vbdr_estimate_host(self._h, C.c_void_p(h_hosts.data_ptr()),
+                                             h_hosts.numel(),
+                                             C.c_void_p(d_hosts_stage.data_ptr()),
+                                             C.c_void_p(d_out_stage.data_ptr()),
+                                             C.c_void_p(h_out.data_ptr()), _stream_ptr(stream)),
+                    "vbdr_estimate_host")
+
+    # --------------------------------------------------------------- exports
+    def export_ages(self, canonical: bool = False, stream=None):
+        import numpy as np
+        L = self.info()["L"]
+        out = np.empty(self.n_phys * L, dtype=np.uint16)
+        self._check(lib().vbdr_export_ages(self._h, out.ctypes.data_as(C.c_void_p),
+                                           1 if canonical else 0, _stream_ptr(stream)),
+                    "vbdr_export_ages")
+        return out.reshape(self.n_phys, L)
+
+    def export_regmax(self, stream=None):
+        import numpy as np
+        out = np.empty(self.n_phys, dtype=np.uint8)
+        self._check(lib().vbdr_export_regmax(self._h, out.ctypes.data_as(C.c_void_p),
+                                             _stream_ptr(stream)), "vbdr_export_regmax")
+        return out
+
+    def export_pool_sums(self, stream=None):
+        S, V = C.c_uint64(), C.c_uint64()
+        self._check(lib().vbdr_export_pool_sums(self._h, C.byref(S), C.byref(V),
+                                                _stream_ptr(stream)), "vbdr_export_pool_sums")
+        return S.value, V.value
+
+
+# ------------------------------------------------------------ multi-GPU plumbing
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [start, stop) of n units for rank (pairs of a slice, or hosts).
+    Shards differ in size by at most one unit; their union is [0, n)."""
+    base, extra = divmod(n, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def merge_stamps(pool: "VBDR", group=None):
+    """Elementwise max of every rank's stamp words (NCCL allreduce MAX over
+    NVLink).  Correct because every replica holds identical pre-slice state and
+    max picks the newest tick, then the highest rank (the serial max of
+    PAPER.md:184 is commutative and idempotent)."""
+    import torch.distributed as dist
+    if group is None and (not dist.is_available() or not dist.is_initialized()):
+        return
+    if dist.get_world_size(group) <= 1:
+        return
+    dist.all_reduce(pool.sr_view(), op=dist.ReduceOp.MAX, group=group)

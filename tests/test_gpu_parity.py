@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle, element by
+element, on the same seeded synthetic inputs.
+
+Bit-exact: registers M, DR state (layout fast: raw ages vs the serial oracle;
+layout packed: canonical C_k vs the gsmall oracle), pool sums, per-host (S, V).
+fp64 estimates: |gpu - oracle| <= 1e-9 * max(|oracle|, C * E_s / g).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1810_13132_b200 import VBDR  # noqa: E402
+
+DEV = torch.device("cuda:0")
+TOL = 1e-9
+
+
+def dev_u32(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).reshape(-1).view(np.int32)).to(DEV)
+
+
+def oracle_pool_sums(M: np.ndarray, L: int):
+    """S_tot = sum_j 2^(L - M_j) and V_tot = #{M_j = 0}, exact integers."""
+    counts = np.bincount(M, minlength=L + 1).astype(object)
+    S = sum(int(counts[r]) << (L - r) for r in range(L + 1))
+    return S, int(counts[0])
+
+
+def check_estimates(gpu, want, Es_over_g_C):
+    floor = np.maximum(np.abs(want), Es_over_g_C)
+    bad = np.abs(gpu - want) > TOL * np.maximum(floor, 1e-300)
+    assert not bad.any(), (np.flatnonzero(bad)[:5], gpu[bad][:5], want[bad][:5])
+
+
+def est_floor(ref: oracle.Pool, M, hosts):
+    """C * E_s / g per host (the scale of the cancelling vHLL terms)."""
+    cfg = ref.cfg
+    Z, V = ref.host_sums(M, hosts)
+    g, z = cfg.g, cfg.z
+    C = (z * g) / (z - g)
+    Es = oracle.alpha(g) * g * g / Z
+    lc = (Es <= 2.5 * g) & (V > 0)
+    Es = np.where(lc, g * np.log(g / np.maximum(V, 1).astype(float)), Es)
+    return C * Es / g
+
+
+def compare_boundary(pool, ref: oracle.Pool, refs_other, hosts_np, hosts_dev, window_pairs,
+                     check_ages=True, check_est=True):
+    cfg = ref.cfg
+    M = ref.readout()
+    got = pool.export_regmax()
+    assert np.array_equal(got, M), "regmax != oracle Alg.2 readout"
+    for o in refs_other:
+        assert np.array_equal(o.readout(), M)
+    if window_pairs is not None:
+        Mstar = oracle.rebuild(window_pairs, cfg.b, cfg.L, cfg.z, cfg.A0, cfg.A1)
+        assert np.array_equal(got, Mstar), "regmax != rebuild from scratch"
+    if check_ages:
+        if pool.layout == "fast":
+            assert np.array_equal(pool.export_ages(), ref.drv()), "DR ages"
+        else:
+            assert np.array_equal(pool.export_ages(canonical=True), ref.ck().astype(np.uint16)), "C_k"
+    assert pool.export_pool_sums() == oracle_pool_sums(M, cfg.L)
+    if hosts_np is not None:
+        S, V = pool.host_sums(hosts_dev)
+        Z, Vo = ref.host_sums(M, hosts_np)
+        assert np.array_equal(V.cpu().numpy().astype(np.uint64), Vo)
+        assert np.array_equal(S.cpu().numpy().astype(np.float64) * 2.0 ** -cfg.L, Z)
+        if check_est:
+            est = pool.estimate(hosts_dev).cpu().numpy()
+            want = ref.estimate(M, hosts_np)
+            check_estimates(est, want, est_floor(ref, M, hosts_np))
+
+
+@pytest.mark.parametrize("layout", ["fast", "packed"])
+@pytest.mark.parametrize("scan_mode", [1, 2])
+def test_tiny_every_boundary(layout, scan_mode):
+    """configs[0] 'tiny': 10k pairs/slice, 64 hosts, m=32, 2^12 BDRs, k=4."""
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    variant = "serial" if layout == "fast" else "gsmall"
+    ref = oracle.Pool(cfg, variant)
+    others = [oracle.Pool(cfg, v) for v in ("gfast", "gsmall" if layout == "fast" else "serial")]
+    pool = VBDR(32, 4, 1 << 12, layout=layout, scan_mode=scan_mode, device=DEV)
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    slices = []
+    # before the first slide everything estimates 0 (empty window)
+    assert (pool.estimate(hosts).cpu().numpy() == 0).all()
+    for t in range(12):
+        pairs = synth.generate(tr, t)
+        slices.append(pairs)
+        # several batches per slice, odd sizes (ragged tails)
+        for a, b in ((0, 3), (3, 4001), (4001, 10_000)):
+            pool.scan_slice(dev_u32(pairs[a:b]))
+        pool.slide()
+        for p in [ref] + others:
+            p.slice(pairs)
+        compare_boundary(pool, ref, others, hosts_np, hosts,
+                         np.concatenate(slices[max(0, t - 3):t + 1]))
+
+
+@pytest.mark.parametrize("layout", ["fast", "packed"])
+@pytest.mark.parametrize("k,m,n_phys", [(1, 2, 64), (3, 16, 1 << 10), (7, 64, 1 << 14),
+                                        (15, 8, 1 << 8), (60, 256, 1 << 16), (300, 4, 1 << 9)])
+def test_configs_sweep_with_empty_slices(layout, k, m, n_phys):
+    """Edge cases: k = 1 (discrete window), k = 2^zb - 1, big k (zb up to 9),
+    g < 32 (several hosts per warp), empty slices, tiny pools."""
+    b = m.bit_length() - 1
+    tr = synth.TraceConfig("sweep", hosts=200, pairs_per_slice=3001, U0=3000, seed=k * 7 + m)
+    cfg = oracle.PoolConfig(b=b, k=k, z=n_phys)
+    if layout == "packed" and (1 << cfg.zb) - 2 < k:
+        cfg = oracle.PoolConfig(b=b, k=k, z=n_phys, zb=cfg.zb + 1)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(m, k, n_phys, layout=layout, device=DEV)
+    assert pool.info()["zbits"] == cfg.zb
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    n_slices = min(2 * k + 5, 40)
+    slices = []
+    for t in range(n_slices):
+        pairs = synth.generate(tr, t) if t % 4 != 2 else np.zeros((0, 2), np.uint32)
+        slices.append(pairs)
+        if len(pairs):
+            pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+        if t % 3 == 0 or t == n_slices - 1:
+            compare_boundary(pool, ref, [], hosts_np, hosts,
+                             np.concatenate(slices[max(0, t - k + 1):t + 1]))
+
+
+@pytest.mark.parametrize("layout", ["fast", "packed"])
+def test_long_run_saturation(layout):
+    """>= 1000 slices of 'tiny' shape: long-run ageing and DR saturation."""
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(32, 4, 1 << 12, layout=layout, device=DEV)
+    tr = synth.TraceConfig("long", hosts=64, pairs_per_slice=600, U0=4000, seed=99)
+    for t in range(1030):
+        pairs = synth.generate(tr, t) if t % 50 < 45 else np.zeros((0, 2), np.uint32)
+        if len(pairs):
+            pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+        if t % 257 == 0 or t >= 1025:
+            compare_boundary(pool, ref, [], None, None, None)
+    assert pool.info()["slices_closed"] == 1030
+
+
+def test_negative_control_skipped_slide_breaks_parity():
+    """a pipeline that skips one slide must fail the comparison."""
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial")
+    pool = VBDR(32, 4, 1 << 12, device=DEV)
+    for t in range(6):
+        pairs = synth.generate(tr, t)
+        pool.scan_slice(dev_u32(pairs))
+        if t != 3:
+            pool.slide()
+        ref.slice(pairs)
+    assert not np.array_equal(pool.export_ages(), ref.drv())
+
+
+def test_order_split_and_duplicates_give_identical_state():
+    tr = synth.CONFIGS["tiny"]
+    a = VBDR(32, 4, 1 << 12, device=DEV)
+    b = VBDR(32, 4, 1 << 12, device=DEV, scan_mode=2)
+    rng = np.random.default_rng(0)
+    for t in range(5):
+        pairs = synth.generate(tr, t)
+        a.scan_slice(dev_u32(pairs))
+        shuffled = np.concatenate([pairs, pairs[:999]])[rng.permutation(len(pairs) + 999)]
+        for part in np.array_split(shuffled, 7):
+            b.scan_slice(dev_u32(part))
+        a.slide()
+        b.slide()
+        assert np.array_equal(a.export_ages(), b.export_ages())
+        assert np.array_equal(a.export_regmax(), b.export_regmax())
+
+
+def test_host_buffer_path_matches_device_path():
+    """vbdr_scan_slice_host / vbdr_estimate_host (the end-to-end entry points)."""
+    tr = synth.CONFIGS["tiny"]
+    a = VBDR(32, 4, 1 << 12, device=DEV)
+    b = VBDR(32, 4, 1 << 12, device=DEV)
+    hosts_np = tr.host_ids()
+    stage = torch.empty(2 * 1000, dtype=torch.int32, device=DEV)  # forces 10+ chunks
+    hstage = torch.empty(len(hosts_np), dtype=torch.int32, device=DEV)
+    ostage = torch.empty(len(hosts_np), dtype=torch.float64, device=DEV)
+    h_hosts = torch.from_numpy(hosts_np.view(np.int32)).pin_memory()
+    h_out = torch.empty(len(hosts_np), dtype=torch.float64).pin_memory()
+    for t in range(6):
+        pairs = synth.generate(tr, t)
+        a.scan_slice(dev_u32(pairs))
+        b.scan_slice_host(torch.from_numpy(pairs.reshape(-1).view(np.int32)).pin_memory(), stage)
+        a.slide()
+        b.slide()
+        b.estimate_host(h_hosts, hstage, ostage, h_out)
+        torch.cuda.synchronize()
+        want = a.estimate(dev_u32(hosts_np)).cpu().numpy()
+        assert np.array_equal(h_out.numpy(), want)
+        assert np.array_equal(a.export_ages(), b.export_ages())
+
+
+def test_synth_cuda_twin_matches_numpy():
+    for name in ("tiny", "caida"):
+        tr = synth.CONFIGS[name]
+        dt = synth.DeviceTrace(tr, DEV)
+        for t, start, count in ((0, 0, 10_000), (3, 123_457, 40_001)):
+            got = dt.generate(t, start, count).cpu().numpy().view(np.uint32).reshape(-1, 2)
+            assert np.array_equal(got, synth.generate(tr, t, start, count))
+
+
+@pytest.mark.parametrize("layout", ["fast", "packed"])
+def test_caida_full_size(layout):
+    """configs[1] 'caida' at full size (5M pairs/slice, 2^22 BDRs, m=128, k=5,
+    500k hosts) in the launch configuration bench.py times: every register,
+    the pool sums and all 500k host sums bit-exact, all estimates to 1e-9,
+    DR state on a sample of BDRs, at several boundaries including a full window."""
+    tr = synth.CONFIGS["caida"]
+    cfg = oracle.PoolConfig(b=7, k=5, z=1 << 22)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(128, 5, 1 << 22, layout=layout, device=DEV)
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    rng = np.random.default_rng(5)
+    sample = np.sort(rng.choice(cfg.z, size=200_000, replace=False))
+    for t in range(7):
+        pairs = synth.generate(tr, t)  # numpy twin: the oracle never sees GPU-made data
+        pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+        if t in (0, 4, 6):
+            M = ref.readout()
+            assert np.array_equal(pool.export_regmax(), M)
+            assert pool.export_pool_sums() == oracle_pool_sums(M, cfg.L)
+            if layout == "fast":
+                assert np.array_equal(pool.export_ages()[sample], ref.drv()[sample])
+            else:
+                assert np.array_equal(pool.export_ages(canonical=True)[sample], ref.ck().astype(np.uint16)[sample])
+            S, V = pool.host_sums(hosts)
+            Z, Vo = ref.host_sums(M, hosts_np)
+            assert np.array_equal(V.cpu().numpy().astype(np.uint64), Vo)
+            assert np.array_equal(S.cpu().numpy().astype(np.float64) * 2.0 ** -cfg.L, Z)
+            est = pool.estimate(hosts).cpu().numpy()
+            check_estimates(est, ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
