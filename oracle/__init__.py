@@ -286,7 +286,7 @@ class Pool:
 
     def ck(self) -> np.ndarray:
         """Canonical state C_k[j][r] = min(DR, k)."""
-        return np.minimum(self.drv(), self.cfg.k).astype(np.uint8)
+        return np.minimum(self.drv(), self.cfg.k).astype(np.uint16)
 
     def gather(self, M: np.ndarray, aip: int) -> np.ndarray:
         M = np.ascontiguousarray(M, dtype=np.uint8)
