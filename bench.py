@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--config", default="caida", choices=list(WORKLOADS))
     ap.add_argument("--layout", default="fast", choices=["fast", "packed"])
     ap.add_argument("--scan-mode", type=int, default=0)
+    ap.add_argument("--est-lanes", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -68,6 +69,26 @@ def peaks():
         return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+CEIL_SRC = "profiles/ceilings_b200.json, tools/ubench_gather.cu"
+
+
+def ceilings():
+    with open(os.path.join(ROOT, "profiles", "ceilings_b200.json")) as f:
+        return json.load(f)
+
+
+def load_traffic(config: str, layout: str) -> dict:
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the last
+    committed ncu --set full capture (profiles/traffic.json), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+    except Exception:
+        return {}
+    pre = f"{config}/{layout}/"
+    return {k[len(pre):]: v for k, v in t.items() if k.startswith(pre)}
 
 
 def algorithmic_bytes_per_bdr(layout: str, words: int) -> int:
@@ -235,7 +256,7 @@ def run_vbdr(args):
     tr = synth.CONFIGS[args.config]
     wl = WORKLOADS[args.config]
     pool = VBDR(wl["m"], wl["k"], wl["n_phys"], layout=args.layout, scan_mode=args.scan_mode,
-                device=dev)
+                est_lanes=args.est_lanes, device=dev)
     info = pool.info()
     p0, p1 = shard_range(tr.pairs_per_slice, rank, world)
     h0, h1 = shard_range(tr.hosts, rank, world)
@@ -353,46 +374,41 @@ def run_vbdr(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline of each kernel; the dominant one goes in "roofline"
     hbm, hbm_src = peaks()
+    ceil = ceilings()
     names = ["scan", "merge", "slide", "estimate"]
     kern = {n: float(v) for n, v in zip(names, per_kernel)}
+    traffic = load_traffic(args.config, args.layout)
     slide_bytes = algorithmic_bytes_per_bdr(args.layout, info["words"]) * wl["n_phys"]
     slide_gbs = slide_bytes / (kern["slide"] * 1e-3) / 1e9
-    pairs_local = n_local
+    regmax_mib = wl["n_phys"] >> 20
+    tab = "4MiB" if regmax_mib <= 4 else "64MiB" if regmax_mib <= 64 else "256MiB"
+    sr_mib = 4 * wl["n_phys"] >> 20
+    red_tab = "16MiB" if sr_mib <= 16 else "48MiB" if sr_mib <= 48 else "256MiB" \
+        if sr_mib <= 256 else "1024MiB"
+    gathers = (h1 - h0) * wl["m"]
+    g_rate = gathers / (kern["estimate"] * 1e-3) / 1e9
+    scan_rate = n_local / (kern["scan"] * 1e-3) / 1e9
     kernels = {
-        "scan": {"ms": kern["scan"], "mpairs_s": pairs_local / (kern["scan"] * 1e-3) / 1e6,
-                 "bound": "l2_atomic", "bytes_per_pair": 8},
+        "scan": {"ms": kern["scan"], "bound": "l2_atomic", "achieved": round(scan_rate, 2),
+                 "peak": ceil["red_max_u32_Gps"][red_tab], "unit": "Gpairs/s",
+                 "frac": round(scan_rate / ceil["red_max_u32_Gps"][red_tab], 4),
+                 "traffic": traffic.get("scan"),
+                 "peak_source": f"random atomicMax ceiling, {red_tab} array ({CEIL_SRC})"},
         "merge": {"ms": kern["merge"]},
-        "slide": {"ms": kern["slide"], "bound": "hbm", "bytes": slide_bytes,
-                  "achieved_gbs": slide_gbs, "frac": slide_gbs / hbm},
-        "estimate": {"ms": kern["estimate"], "hosts": h1 - h0,
-                     "gathers_per_s": (h1 - h0) * wl["m"] / (kern["estimate"] * 1e-3)},
+        "slide": {"ms": kern["slide"], "bound": "hbm", "achieved": round(slide_gbs, 1),
+                  "peak": hbm, "unit": "GB/s", "frac": round(slide_gbs / hbm, 4),
+                  "traffic": traffic.get("slide"), "algorithmic_bytes": slide_bytes,
+                  "peak_source": hbm_src},
+        "estimate": {"ms": kern["estimate"], "bound": "l2_gather", "achieved": round(g_rate, 2),
+                     "peak": ceil["ldg_gather_1B_Gps"][tab], "unit": "Ggathers/s",
+                     "frac": round(g_rate / ceil["ldg_gather_1B_Gps"][tab], 4),
+                     "traffic": traffic.get("estimate"), "hosts": h1 - h0, "gathers": gathers,
+                     "peak_source": f"random 1-byte LDG gather ceiling, {tab} table ({CEIL_SRC})"},
     }
     dominant = max(("scan", "slide", "estimate"), key=lambda n: kern[n])
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get(f"{args.config}/{args.layout}/{dominant}")
-        except Exception:
-            traffic = None
-    if dominant == "slide":
-        roof = {"kernel": "slide", "bound": "hbm", "achieved": round(slide_gbs, 1),
-                "peak": hbm, "unit": "GB/s", "frac": round(slide_gbs / hbm, 4), "traffic": traffic,
-                "peak_source": hbm_src}
-    else:
-        # scan / estimate: the algorithmic DRAM bytes (8 B per pair in, 4 B per
-        # host in + 8 B out) -- a strict HBM roofline; their real limit is the
-        # L2 random-access rate (DESIGN.md s.6)
-        if dominant == "scan":
-            byts = 8 * pairs_local
-        else:
-            byts = 12 * (h1 - h0)
-        ach = byts / (kern[dominant] * 1e-3) / 1e9
-        roof = {"kernel": dominant, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
-                "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": traffic,
-                "peak_source": hbm_src}
+    roof = {"kernel": dominant, **{k: v for k, v in kernels[dominant].items() if k != "ms"}}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -409,12 +425,13 @@ def run_vbdr(args):
                    "pairs_per_slice": tr.pairs_per_slice, "hosts": tr.hosts,
                    "parallelism": f"pairs+hosts sharded x{world}, allreduce(MAX) merge",
                    "l2": f"flushed before every step ({args.flush_mib} MiB write)",
-                   "scan_mode": args.scan_mode},
+                   "scan_mode": args.scan_mode, "est_lanes": args.est_lanes},
         "scan_mpairs_s": round(tr.pairs_per_slice / (kern["scan"] * 1e-3) / 1e6, 2),
         "slide_ms": round(kern["slide"], 5), "estimate_ms": round(kern["estimate"], 5),
         "merge_ms": round(kern["merge"], 5),
         "kernels": kernels,
         "roofline": roof,
+        "roofline_slide_hbm": {k: v for k, v in kernels["slide"].items() if k != "ms"},
         "gpu_launches": int(launches),
         "clocks": clk,
         "e2e": e2e,

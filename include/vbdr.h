@@ -78,10 +78,14 @@ typedef struct {
     uint32_t rank_cap;
     /* layout: vbdr_layout. */
     uint32_t layout;
-    /* scan_mode: 0 = default; 1 = plain atomic per pair; 2 = load-check, skip
-     * the atomic when the stored value already dominates; 3 = warp-aggregated
-     * atomics (__match_any_sync).  All modes give bit-identical state. */
+    /* scan_mode: 0 = default; 1 = plain atomic per pair; 2 = L2 load-check,
+     * skip the atomic when the stored value already dominates; 3 = reserved
+     * (runs as 1); 4 = L1-cached load-check.  All modes give bit-identical
+     * state (stored values only move one way within a slice). */
     uint32_t scan_mode;
+    /* est_lanes: lanes cooperating on one host in vbdr_estimate (1, 2, 4, 8,
+     * 16 or 32; 0 = auto).  Tuning only; results are identical. */
+    uint32_t est_lanes;
 } vbdr_config;
 
 /* Derived sizes and the layout of the state buffer (byte offsets from the

@@ -7,9 +7,14 @@
 //   E_s = alpha_g g^2 / (S 2^-L); linear counting g ln(g/V) if E_s <= 2.5 g
 //   and V > 0 (R#16); est = max(0, C (E_s/g - E_tot/z)) (vHLL, PAPER.md:214,
 //   R#15), E_tot from the pool sums the slide produced.
-// G lanes cooperate on one host (G = min(g, 32)); each lane owns the virtual
-// indices i = sub + q G and keeps s1 = H(i, 2^32, A0) (Alg.3) in
-// registers for the whole kernel.
+//
+// G lanes cooperate on one host (a "group"); lane `sub` of the group owns the
+// virtual indices i = sub + G q.  s1[i] = H(i, 2^32, A0) (Alg.3) is
+// the same for every host, so the block tabulates it once in shared memory.
+// The gathers are random 1-byte loads from regmax (L2-resident up to 2^26
+// BDRs): the kernel is bound by the SM's L1-to-L2 request rate, one sector
+// per gather; U independent gathers per lane keep
+// enough requests in flight.
 #include "vbdr_dev.cuh"
 
 using namespace vbdr_dev;
@@ -18,20 +23,24 @@ using vbdr_launch::EstParams;
 namespace {
 
 constexpr int kThreads = 256;
+constexpr uint32_t kS1SmemMax = 8192;  // g up to this uses the shared table
 
-__device__ __forceinline__ double hll_finish(double agg_over, double D, double lc, uint64_t V,
+__device__ __forceinline__ double hll_finish(double agg, double D, double lc, uint64_t V,
                                              double s) {
-  double E = __ddiv_rn(agg_over, D);
+  double E = __ddiv_rn(agg, D);
   if (E <= lc && V > 0) E = __dmul_rn(s, log(__ddiv_rn(s, (double)V)));
   return E;
 }
 
-// NQ > 0: compile-time indices per lane; NQ == 0: runtime g/32 (g > 256).
-template <int G, int NQ, bool SUMS>
+template <int G, int U, bool SUMS, bool SMEM>
 __global__ void __launch_bounds__(kThreads)
 k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *__restrict__ out,
            unsigned long long *__restrict__ outS, uint32_t *__restrict__ outV) {
+  extern __shared__ uint32_t s1tab[];
   __shared__ double s_etot_z;  // E_tot / z
+  if constexpr (SMEM) {
+    for (uint32_t i = threadIdx.x; i < e.g; i += kThreads) s1tab[i] = fmix32(i ^ e.A0);
+  }
   if (!SUMS && threadIdx.x == 0) {
     const unsigned long long St = e.acc[0], Vt = e.acc[1];
     const double D = __dmul_rn((double)St, e.inv2L);  // exact: St <= 2^53
@@ -41,37 +50,30 @@ k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t sub = lane & (G - 1u);
-  const uint32_t grp = lane / G;
-  constexpr uint32_t HPW = 32 / G;  // hosts per warp
-  constexpr int NQR = NQ > 0 ? NQ : 1;
-  uint32_t s1[NQR];
-#pragma unroll
-  for (int q = 0; q < NQR; ++q) s1[q] = fmix32((sub + (uint32_t)q * G) ^ e.A0);
-  const uint32_t nq_rt = e.g / G;
+  const uint64_t tid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  const uint64_t warp_first = (tid & ~uint64_t(31)) / G;  // first group of this warp
+  const uint64_t group = tid / G;
+  const uint64_t ngroups = ((uint64_t)gridDim.x * kThreads) / G;
+  const uint32_t per_lane = e.g / G;
 
-  const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
-  for (uint64_t base = warp * HPW; base < n; base += nwarps * HPW) {
-    const uint64_t h = base + grp;
+  for (uint64_t r = 0; warp_first + r < n; r += ngroups) {  // warp-uniform
+    const uint64_t h = group + r;
     const bool valid = h < n;
     const uint32_t aip = valid ? __ldg(hosts + h) : 0u;
     unsigned long long S = 0ull;
     uint32_t V = 0u;
-    if constexpr (NQ > 0) {
-      uint32_t M[NQ];
+    for (uint32_t q = 0; q < per_lane; q += U) {
+      uint32_t M[U];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) M[q] = __ldg(e.regmax + (fmix32(aip ^ s1[q]) & e.mask));
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        S += 1ull << (e.L - M[q]);
-        V += M[q] == 0u;
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = sub + (uint32_t)G * (q + (uint32_t)u);
+        const uint32_t s1 = SMEM ? s1tab[i] : fmix32(i ^ e.A0);
+        M[u] = __ldg(e.regmax + (fmix32(aip ^ s1) & e.mask));
       }
-    } else {
-      for (uint32_t q = 0; q < nq_rt; ++q) {
-        const uint32_t s = fmix32((sub + q * G) ^ e.A0);
-        const uint32_t M = __ldg(e.regmax + (fmix32(aip ^ s) & e.mask));
-        S += 1ull << (e.L - M);
-        V += M == 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        S += 1ull << (e.L - M[u]);
+        V += M[u] == 0u;
       }
     }
 #pragma unroll
@@ -94,49 +96,70 @@ k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *
   }
 }
 
-uint32_t grid_for_hosts(uint64_t n, uint32_t hpw) {
-  static int sms = 0;
-  if (sms == 0) {
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
   }
-  const uint64_t warps = (n + hpw - 1) / hpw;
-  const uint64_t need = (warps * 32 + kThreads - 1) / kThreads;
-  const uint64_t cap = (uint64_t)sms * 8;
-  const uint64_t g = need < cap ? need : cap;
-  return (uint32_t)(g ? g : 1);
+  return n;
 }
 
-template <int G, int NQ>
+template <int G, int U, bool SMEM>
 cudaError_t run(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
                 unsigned long long *outS, uint32_t *outV, cudaStream_t s) {
-  const uint32_t grid = grid_for_hosts(n, 32 / G);
-  if (outS != nullptr)
-    k_estimate<G, NQ, true><<<grid, kThreads, 0, s>>>(e, hosts, n, out, outS, outV);
-  else
-    k_estimate<G, NQ, false><<<grid, kThreads, 0, s>>>(e, hosts, n, out, outS, outV);
+  const size_t smem = SMEM ? (size_t)e.g * 4 : 0;
+  auto kern = outS ? k_estimate<G, U, true, SMEM> : k_estimate<G, U, false, SMEM>;
+  // occupancy is cached while the s1 table is too small to limit it (g <= 1024)
+  static int per_sm_cache[2] = {0, 0};
+  int local = 0;
+  int &per_sm = smem <= 4096 ? per_sm_cache[outS ? 1 : 0] : local;
+  if (per_sm == 0 &&
+      (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess ||
+       per_sm <= 0))
+    per_sm = 1;
+  const uint64_t resident = (uint64_t)per_sm * sm_count();
+  const uint64_t need = (n * G + kThreads - 1) / kThreads;
+  const uint64_t grid = need < resident ? need : resident;
+  kern<<<(uint32_t)(grid ? grid : 1), kThreads, smem, s>>>(e, hosts, n, out, outS, outV);
   return cudaGetLastError();
+}
+
+template <int G>
+cudaError_t run_g(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
+                  unsigned long long *outS, uint32_t *outV, cudaStream_t s) {
+  const uint32_t per_lane = e.g / G;
+  const bool smem = e.g <= kS1SmemMax;
+  if (per_lane >= 8)
+    return smem ? run<G, 8, true>(e, hosts, n, out, outS, outV, s)
+                : run<G, 8, false>(e, hosts, n, out, outS, outV, s);
+  if (per_lane == 4) return run<G, 4, true>(e, hosts, n, out, outS, outV, s);
+  if (per_lane == 2) return run<G, 2, true>(e, hosts, n, out, outS, outV, s);
+  return run<G, 1, true>(e, hosts, n, out, outS, outV, s);
 }
 
 }  // namespace
 
 namespace vbdr_launch {
 
+// Lanes per host: `lanes` if given (a power of two <= min(g, 32)), else 8
+// (best on the caida sweep, profiles/r01_sweep_caida.jsonl), capped at g.
 cudaError_t estimate(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
                      unsigned long long *outS, uint32_t *outV, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  switch (e.g) {
-    case 2: return run<2, 1>(e, hosts, n, out, outS, outV, s);
-    case 4: return run<4, 1>(e, hosts, n, out, outS, outV, s);
-    case 8: return run<8, 1>(e, hosts, n, out, outS, outV, s);
-    case 16: return run<16, 1>(e, hosts, n, out, outS, outV, s);
-    case 32: return run<32, 1>(e, hosts, n, out, outS, outV, s);
-    case 64: return run<32, 2>(e, hosts, n, out, outS, outV, s);
-    case 128: return run<32, 4>(e, hosts, n, out, outS, outV, s);
-    case 256: return run<32, 8>(e, hosts, n, out, outS, outV, s);
-    default: return run<32, 0>(e, hosts, n, out, outS, outV, s);
+  uint32_t G = e.lanes ? e.lanes : 8u;
+  if (G > e.g) G = e.g;
+  if (G > 32) G = 32;
+  switch (G) {
+    case 1: return run_g<1>(e, hosts, n, out, outS, outV, s);
+    case 2: return run_g<2>(e, hosts, n, out, outS, outV, s);
+    case 4: return run_g<4>(e, hosts, n, out, outS, outV, s);
+    case 8: return run_g<8>(e, hosts, n, out, outS, outV, s);
+    case 16: return run_g<16>(e, hosts, n, out, outS, outV, s);
+    case 32: return run_g<32>(e, hosts, n, out, outS, outV, s);
+    default: return cudaErrorInvalidValue;
   }
 }
 

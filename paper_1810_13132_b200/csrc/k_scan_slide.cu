@@ -36,6 +36,11 @@ __device__ __forceinline__ void record(uint32_t aip, uint32_t bip, const DevPara
     if constexpr (MODE == 2) {
       if (ld_relaxed(a) >= val) return;  // stored value dominates: max is a no-op
     }
+    if constexpr (MODE == 4) {
+      // L1-cached check: a stale line can only hold a smaller (older) value,
+      // so skipping when it dominates is still exact
+      if (__ldca(a) >= val) return;
+    }
     atomicMax(a, val);
   } else {
     // SetDR(DRV[LBP1(bip')]) = clear one zb-bit field
@@ -47,6 +52,11 @@ __device__ __forceinline__ void record(uint32_t aip, uint32_t bip, const DevPara
     uint32_t *a = p.drv + (uint64_t)w * p.n_phys + pidx;
     if constexpr (MODE == 2) {
       if ((ld_relaxed(a) & fm) == 0u) return;  // already zero
+    }
+    if constexpr (MODE == 4) {
+      // within a slice fields only go to zero: a stale (older) line showing
+      // zero is still zero now
+      if ((__ldca(a) & fm) == 0u) return;
     }
     atomicAnd(a, ~fm);
   }
@@ -207,10 +217,20 @@ int sm_count() {
   return n;
 }
 
-uint32_t grid_for(uint64_t work, int blocks_per_sm) {
+// Persistent grid: as many blocks as can be resident (occupancy of this
+// kernel x SM count), never more than the work needs.
+template <typename K>
+uint32_t grid_for(K kernel, uint64_t work) {
+  static int resident = 0;  // one static per kernel instantiation
+  if (resident == 0) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0) != cudaSuccess ||
+        per_sm <= 0)
+      per_sm = 1;
+    resident = per_sm * sm_count();
+  }
   const uint64_t need = (work + kThreads - 1) / kThreads;
-  const uint64_t cap = (uint64_t)sm_count() * blocks_per_sm;
-  uint64_t g = need < cap ? need : cap;
+  const uint64_t g = need < (uint64_t)resident ? need : (uint64_t)resident;
   return (uint32_t)(g ? g : 1);
 }
 
@@ -234,7 +254,7 @@ cudaError_t dispatch_zb(uint32_t zb, Args &&...args) {
 template <int ZB>
 struct InitFn {
   static cudaError_t run(const DevParams &p, bool fast, cudaStream_t s) {
-    k_init<ZB><<<grid_for(p.n_phys >> 2, 8), kThreads, 0, s>>>(p, fast);
+    k_init<ZB><<<grid_for(k_init<ZB>, p.n_phys >> 2), kThreads, 0, s>>>(p, fast);
     return cudaGetLastError();
   }
 };
@@ -246,24 +266,37 @@ struct SlideFn {
     uint32_t addk = 0;
     for (uint32_t f = 0; f < Swar<ZB>::F; f += 2) addk |= ((1u << ZB) - p.k) << (ZB * f);
     const uint32_t slot = p.tick & 1u;
-    const uint32_t grid = grid_for(p.n_phys >> 2, 8);
+    const uint64_t work = p.n_phys >> 2;
     if (fast)
-      k_slide<true, ZB><<<grid, kThreads, 0, s>>>(p, addk, slot);
+      k_slide<true, ZB><<<grid_for(k_slide<true, ZB>, work), kThreads, 0, s>>>(p, addk, slot);
     else
-      k_slide<false, ZB><<<grid, kThreads, 0, s>>>(p, addk, slot);
+      k_slide<false, ZB><<<grid_for(k_slide<false, ZB>, work), kThreads, 0, s>>>(p, addk, slot);
     return cudaGetLastError();
   }
 };
 
+template <bool FAST, int ZB>
+cudaError_t launch_scan(const DevParams &p, int mode, const uint4 *pairs2, uint64_t n2,
+                        const uint32_t *tail, cudaStream_t s) {
+  const uint64_t work = n2 ? n2 : 1;
+  switch (mode) {
+    case 2:
+      k_scan<FAST, ZB, 2><<<grid_for(k_scan<FAST, ZB, 2>, work), kThreads, 0, s>>>(pairs2, n2, tail, p);
+      break;
+    case 4:
+      k_scan<FAST, ZB, 4><<<grid_for(k_scan<FAST, ZB, 4>, work), kThreads, 0, s>>>(pairs2, n2, tail, p);
+      break;
+    default:
+      k_scan<FAST, ZB, 1><<<grid_for(k_scan<FAST, ZB, 1>, work), kThreads, 0, s>>>(pairs2, n2, tail, p);
+  }
+  return cudaGetLastError();
+}
+
 template <int ZB>
 struct ScanPackedFn {
   static cudaError_t run(const DevParams &p, int mode, const uint4 *pairs2, uint64_t n2,
-                         const uint32_t *tail, uint32_t grid, cudaStream_t s) {
-    if (mode == 2)
-      k_scan<false, ZB, 2><<<grid, kThreads, 0, s>>>(pairs2, n2, tail, p);
-    else
-      k_scan<false, ZB, 1><<<grid, kThreads, 0, s>>>(pairs2, n2, tail, p);
-    return cudaGetLastError();
+                         const uint32_t *tail, cudaStream_t s) {
+    return launch_scan<false, ZB>(p, mode, pairs2, n2, tail, s);
   }
 };
 
@@ -285,15 +318,8 @@ cudaError_t scan(const DevParams &p, bool fast, int mode, const uint32_t *pairs,
   const uint64_t n2 = n >> 1;
   const uint32_t *tail = (n & 1u) ? pairs + 2 * (n - 1) : nullptr;
   const uint4 *pairs2 = reinterpret_cast<const uint4 *>(pairs);
-  const uint32_t grid = grid_for(n2 ? n2 : 1, 8);
-  if (fast) {
-    if (mode == 2)
-      k_scan<true, 1, 2><<<grid, kThreads, 0, s>>>(pairs2, n2, tail, p);
-    else
-      k_scan<true, 1, 1><<<grid, kThreads, 0, s>>>(pairs2, n2, tail, p);
-    return cudaGetLastError();
-  }
-  return dispatch_zb<ScanPackedFn>(p.zb, p, mode, pairs2, n2, tail, grid, s);
+  if (fast) return launch_scan<true, 1>(p, mode, pairs2, n2, tail, s);
+  return dispatch_zb<ScanPackedFn>(p.zb, p, mode, pairs2, n2, tail, s);
 }
 
 }  // namespace vbdr_launch

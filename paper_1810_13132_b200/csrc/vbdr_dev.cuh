@@ -108,6 +108,7 @@ struct EstParams {
   const uint8_t *regmax;
   const unsigned long long *acc;  // (S_tot, V_tot) of the closed tick
   uint32_t mask, A0, L, g;
+  uint32_t lanes;     // lanes per host (0 = default)
   double inv2L;       // 2^-L
   double agg;         // alpha_g * g * g
   double lc_g;        // 2.5 * g

@@ -63,7 +63,9 @@ std::string plan(const vbdr_config *c, vbdr_config *norm, Plan *pl) {
     n.seed_a1 = 0x5EED0002u;
   }
   if (n.layout > 1) return "layout must be 0 (fast) or 1 (packed)";
-  if (n.scan_mode > 3) return "scan_mode must be 0..3";
+  if (n.scan_mode > 4) return "scan_mode must be 0..4";
+  if (n.est_lanes > 32 || (n.est_lanes & (n.est_lanes - 1)))
+    return "est_lanes must be 0 or a power of two <= 32";
   if (n.m < 2 || !is_pow2(n.m)) return "m must be a power of two >= 2";
   if (n.k < 1) return "k must be >= 1";
   if (n.n_phys < 4 || !is_pow2(n.n_phys) || n.n_phys > (1ull << 32))
@@ -126,6 +128,14 @@ vbdr_status check_async(vbdr *h, const char *where) {
 
 cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// scan_mode 0 picks the default (2: L2 load-check, fastest on the caida sweep,
+// profiles/r01_sweep_caida.jsonl); 3 (warp aggregation) is not built and runs as 1.
+int scan_mode(const vbdr *h) {
+  const uint32_t m = h->cfg.scan_mode;
+  if (m == 0) return 2;
+  return m == 3 ? 1 : (int)m;
+}
+
 vbdr_launch::EstParams est_params(const vbdr *h) {
   vbdr_launch::EstParams e{};
   const uint32_t closed = h->p.tick - 1u;  // tick of the last boundary (0 = none)
@@ -135,6 +145,7 @@ vbdr_launch::EstParams est_params(const vbdr *h) {
   e.A0 = h->p.A0;
   e.L = h->p.L;
   e.g = h->cfg.m;
+  e.lanes = h->cfg.est_lanes;
   e.inv2L = std::ldexp(1.0, -(int)h->p.L);
   const double g = (double)h->cfg.m, z = (double)h->cfg.n_phys;
   e.agg = h->alpha_g * g * g;  // exact: g is a power of two
@@ -270,8 +281,7 @@ vbdr_status vbdr_scan_slice(vbdr_t *h, const uint32_t *d_pairs, uint64_t n_pairs
   if (!d_pairs || (reinterpret_cast<uintptr_t>(d_pairs) & 15u))
     return fail(h, VBDR_EINVAL, "d_pairs must be a 16-byte aligned device pointer");
   if (vbdr_status s = check_async(h, "before scan")) return s;
-  const int mode = h->cfg.scan_mode == 0 ? 1 : (int)h->cfg.scan_mode;
-  const cudaError_t e = vbdr_launch::scan(h->p, h->fast, mode == 3 ? 1 : mode, d_pairs, n_pairs,
+  const cudaError_t e = vbdr_launch::scan(h->p, h->fast, scan_mode(h), d_pairs, n_pairs,
                                           S(stream));
   if (e != cudaSuccess) return cuda_fail(h, e, "scan launch");
   h->info.launches += 1;
@@ -352,8 +362,7 @@ vbdr_status vbdr_scan_slice_host(vbdr_t *h, const uint32_t *h_pairs, uint64_t n_
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_copied[slot], h->copy_stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, h->ev_copied[slot], 0);
     if (e == cudaSuccess) {
-      const int mode = h->cfg.scan_mode == 0 ? 1 : (int)h->cfg.scan_mode;
-      e = vbdr_launch::scan(h->p, h->fast, mode == 3 ? 1 : mode, dst, cnt, cs);
+      e = vbdr_launch::scan(h->p, h->fast, scan_mode(h), dst, cnt, cs);
       h->info.launches += 1;
     }
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_scanned[slot], cs);

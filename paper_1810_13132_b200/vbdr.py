@@ -25,7 +25,8 @@ STATUS = {0: "ok", -1: "EINVAL", -2: "ERANGE", -3: "ESTATE", -4: "ENOMEM", -5: "
 class vbdr_config(C.Structure):
     _fields_ = [("m", C.c_uint32), ("k", C.c_uint32), ("n_phys", C.c_uint64),
                 ("seed_a0", C.c_uint32), ("seed_a1", C.c_uint32), ("zbits", C.c_uint32),
-                ("rank_cap", C.c_uint32), ("layout", C.c_uint32), ("scan_mode", C.c_uint32)]
+                ("rank_cap", C.c_uint32), ("layout", C.c_uint32), ("scan_mode", C.c_uint32),
+                ("est_lanes", C.c_uint32)]
 
 
 class vbdr_info_t(C.Structure):
@@ -83,9 +84,10 @@ def lib():
 
 def make_config(m: int, k: int, n_phys: int, seed_a0: int = 0x5EED0001,
                 seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
-                layout: str | int = "fast", scan_mode: int = 0) -> vbdr_config:
+                layout: str | int = "fast", scan_mode: int = 0,
+                est_lanes: int = 0) -> vbdr_config:
     lay = LAYOUTS[layout] if isinstance(layout, str) else int(layout)
-    return vbdr_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, lay, scan_mode)
+    return vbdr_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, lay, scan_mode, est_lanes)
 
 
 def state_bytes(cfg: vbdr_config) -> int:
@@ -108,12 +110,14 @@ class VBDR:
 
     def __init__(self, m: int, k: int, n_phys: int, *, seed_a0: int = 0x5EED0001,
                  seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
-                 layout: str = "fast", scan_mode: int = 0, device=None, stream=None):
+                 layout: str = "fast", scan_mode: int = 0, est_lanes: int = 0, device=None,
+                 stream=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("VBDR needs a CUDA device (no CPU fallback)")
         self.device = torch.device(device if device is not None else "cuda")
-        self.cfg = make_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, layout, scan_mode)
+        self.cfg = make_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, layout, scan_mode,
+                               est_lanes)
         nbytes = state_bytes(self.cfg)
         with torch.cuda.device(self.device):
             self.state = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -246,14 +250,22 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     return start, start + base + (1 if rank < extra else 0)
 
 
-def merge_stamps(pool: "VBDR", group=None):
-    """Elementwise max of every rank's stamp words (NCCL allreduce MAX over
-    NVLink).  Correct because every replica holds identical pre-slice state and
-    max picks the newest tick, then the highest rank (the serial max of
-    PAPER.md:184 is commutative and idempotent)."""
+def merge_stamps_tensor(sr, group=None):
+    """Elementwise max of every rank's stamp words, in place (allreduce MAX:
+    NCCL over NVLink for device tensors, gloo for host tensors in tests).
+    Correct because every replica holds identical pre-slice state and max picks
+    the newest tick, then the highest rank -- the serial max of PAPER.md:184 is
+    commutative and idempotent, so any split of a slice's pairs over ranks gives
+    the same merged stamps."""
     import torch.distributed as dist
     if group is None and (not dist.is_available() or not dist.is_initialized()):
-        return
+        return sr
     if dist.get_world_size(group) <= 1:
-        return
-    dist.all_reduce(pool.sr_view(), op=dist.ReduceOp.MAX, group=group)
+        return sr
+    dist.all_reduce(sr, op=dist.ReduceOp.MAX, group=group)
+    return sr
+
+
+def merge_stamps(pool: "VBDR", group=None):
+    """merge_stamps_tensor on the pool's stamp array (layout fast)."""
+    return merge_stamps_tensor(pool.sr_view(), group)

@@ -81,15 +81,16 @@ def compare_boundary(pool, ref: oracle.Pool, refs_other, hosts_np, hosts_dev, wi
 
 
 @pytest.mark.parametrize("layout", ["fast", "packed"])
-@pytest.mark.parametrize("scan_mode", [1, 2])
-def test_tiny_every_boundary(layout, scan_mode):
+@pytest.mark.parametrize("scan_mode,est_lanes", [(1, 0), (2, 1), (4, 8), (1, 32), (4, 2)])
+def test_tiny_every_boundary(layout, scan_mode, est_lanes):
     """configs[0] 'tiny': 10k pairs/slice, 64 hosts, m=32, 2^12 BDRs, k=4."""
     tr = synth.CONFIGS["tiny"]
     cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
     variant = "serial" if layout == "fast" else "gsmall"
     ref = oracle.Pool(cfg, variant)
     others = [oracle.Pool(cfg, v) for v in ("gfast", "gsmall" if layout == "fast" else "serial")]
-    pool = VBDR(32, 4, 1 << 12, layout=layout, scan_mode=scan_mode, device=DEV)
+    pool = VBDR(32, 4, 1 << 12, layout=layout, scan_mode=scan_mode, est_lanes=est_lanes,
+                device=DEV)
     hosts_np = tr.host_ids()
     hosts = dev_u32(hosts_np)
     slices = []
@@ -254,3 +255,38 @@ def test_caida_full_size(layout):
             assert np.array_equal(S.cpu().numpy().astype(np.float64) * 2.0 ** -cfg.L, Z)
             est = pool.estimate(hosts).cpu().numpy()
             check_estimates(est, ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
+
+
+@pytest.mark.parametrize("n_ranks", [2, 4, 8])
+def test_loopback_multi_rank_merge(n_ranks):
+    """N virtual ranks on one GPU: each scans a contiguous shard of every slice
+    into its own pool, the stamp arrays merge by elementwise max (what the NCCL
+    allreduce(MAX) does across GPUs), every rank slides; all replicas equal the
+    single-rank pool and the oracle, and host-sharded estimates reassemble."""
+    from paper_1810_13132_b200 import shard_range
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial")
+    ranks = [VBDR(32, 4, 1 << 12, device=DEV) for _ in range(n_ranks)]
+    hosts_np = tr.host_ids()
+    for t in range(7):
+        pairs = synth.generate(tr, t)
+        for r, pool in enumerate(ranks):
+            a, b = shard_range(len(pairs), r, n_ranks)
+            pool.scan_slice(dev_u32(pairs[a:b]))
+        merged = ranks[0].sr_view().clone()
+        for pool in ranks[1:]:
+            merged = torch.maximum(merged, pool.sr_view())
+        for pool in ranks:
+            pool.sr_view().copy_(merged)
+            pool.slide()
+        ref.slice(pairs)
+        for pool in ranks:
+            assert np.array_equal(pool.export_ages(), ref.drv())
+            assert np.array_equal(pool.export_regmax(), ref.readout())
+    M = ref.readout()
+    parts = []
+    for r, pool in enumerate(ranks):
+        h0, h1 = shard_range(len(hosts_np), r, n_ranks)
+        parts.append(pool.estimate(dev_u32(hosts_np[h0:h1])).cpu().numpy())
+    check_estimates(np.concatenate(parts), ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
