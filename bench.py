@@ -91,6 +91,15 @@ def load_traffic(config: str, layout: str) -> dict:
     return {k[len(pre):]: v for k, v in t.items() if k.startswith(pre)}
 
 
+def table1_bits(m: int, k: int) -> dict:
+    """Table 1 with log2(n/g) -> L = 32 - log2(m) and
+    log2(k+1) -> ceil(log2(k+1)): bits per BDR of the paper's three variants."""
+    L = 32 - (m.bit_length() - 1)
+    zb = max(1, (k).bit_length())  # ceil(log2(k+1))
+    lgL = (L - 1).bit_length()     # ceil(log2 L)
+    return {"serial": lgL + L * zb, "gfast": L + L * zb, "gsmall": L * zb}
+
+
 def algorithmic_bytes_per_bdr(layout: str, words: int) -> int:
     """Slide kernel, per physical BDR: read sr (4 B, fast only), read+write W
     packed DRV words (8 W B), write the register value (1 B).  DESIGN.md s.6."""
@@ -425,7 +434,10 @@ def run_vbdr(args):
                    "pairs_per_slice": tr.pairs_per_slice, "hosts": tr.hosts,
                    "parallelism": f"pairs+hosts sharded x{world}, allreduce(MAX) merge",
                    "l2": f"flushed before every step ({args.flush_mib} MiB write)",
-                   "scan_mode": args.scan_mode, "est_lanes": args.est_lanes},
+                   "scan_mode": args.scan_mode, "est_lanes": args.est_lanes,
+                   "zbits": info["zbits"], "words_per_bdr": info["words"],
+                   "bits_per_bdr": (32 if args.layout == "fast" else 0) + 32 * info["words"],
+                   "table1_bits_per_bdr": table1_bits(wl["m"], wl["k"])},
         "scan_mpairs_s": round(tr.pairs_per_slice / (kern["scan"] * 1e-3) / 1e6, 2),
         "slide_ms": round(kern["slide"], 5), "estimate_ms": round(kern["estimate"], 5),
         "merge_ms": round(kern["merge"], 5),
