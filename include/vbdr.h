@@ -86,6 +86,11 @@ typedef struct {
     /* est_lanes: lanes cooperating on one host in vbdr_estimate (1, 2, 4, 8,
      * 16 or 32; 0 = auto).  Tuning only; results are identical. */
     uint32_t est_lanes;
+    /* est_pass_log2: vbdr_estimate gathers from physical ranges of
+     * 2^est_pass_log2 registers, one kernel pass per range, so each pass's
+     * slice of the register array stays L2-resident (0 = auto: 26, i.e. one
+     * pass up to 2^26 BDRs).  Tuning only; results are identical. */
+    uint32_t est_pass_log2;
 } vbdr_config;
 
 /* Derived sizes and the layout of the state buffer (byte offsets from the
@@ -177,6 +182,12 @@ vbdr_status vbdr_info(const vbdr_t *h, vbdr_info_t *info);
  * slice).  mode 1: canonical C_k[j][rho] = min(age, k) at the last boundary
  * (DESIGN.md section 4). */
 vbdr_status vbdr_export_ages(vbdr_t *h, uint16_t *h_ages, int mode, void *stream);
+
+/* SYNC.  vbdr_export_ages for the sampled BDRs d_idx (u64[n_idx], device),
+ * through the caller's device scratch d_scratch (u32[n_idx * words]); h_ages
+ * is u16[n_idx * L].  For pools too large to export whole. */
+vbdr_status vbdr_export_ages_at(vbdr_t *h, const uint64_t *d_idx, uint64_t n_idx,
+                                uint32_t *d_scratch, uint16_t *h_ages, int mode, void *stream);
 
 /* SYNC.  Register values M[j] (u8[n_phys]) of the last boundary. */
 vbdr_status vbdr_export_regmax(vbdr_t *h, uint8_t *h_regmax, void *stream);

@@ -100,6 +100,9 @@ def _declare(L):
         "orc_rebuild": (None, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                u32p, C.c_uint64, u8p]),
         "orc_memory_bits": (C.c_uint64, [C.c_int, C.c_uint32, C.c_uint32]),
+        "orc_estimate_M": (None, [C.c_uint32, C.c_uint32, C.c_uint64, u8p, u32p, C.c_uint64, f64p]),
+        "orc_host_sums_M": (None, [C.c_uint32, C.c_uint32, C.c_uint64, u8p, u32p, C.c_uint64,
+                                   f64p, u64p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -170,6 +173,25 @@ def rebuild(pairs: np.ndarray, b, L, z, A0, A1) -> np.ndarray:
     out = np.zeros(z, dtype=np.uint8)
     lib().orc_rebuild(b, L, A0, A1, z, _ptr(pairs, u32p), pairs.size // 2, _ptr(out, u8p))
     return out
+
+
+def estimate_M(M: np.ndarray, hosts: np.ndarray, b: int, z: int, A0: int = 0x5EED0001):
+    """Per-host estimates from a register array (e.g. a rebuild), no pool."""
+    M = np.ascontiguousarray(M, dtype=np.uint8)
+    hosts = np.ascontiguousarray(hosts, dtype=np.uint32)
+    out = np.empty(hosts.size, dtype=np.float64)
+    lib().orc_estimate_M(b, A0, z, _ptr(M, u8p), _ptr(hosts, u32p), hosts.size, _ptr(out, f64p))
+    return out
+
+
+def host_sums_M(M: np.ndarray, hosts: np.ndarray, b: int, z: int, A0: int = 0x5EED0001):
+    M = np.ascontiguousarray(M, dtype=np.uint8)
+    hosts = np.ascontiguousarray(hosts, dtype=np.uint32)
+    Z = np.empty(hosts.size, dtype=np.float64)
+    V = np.empty(hosts.size, dtype=np.uint64)
+    lib().orc_host_sums_M(b, A0, z, _ptr(M, u8p), _ptr(hosts, u32p), hosts.size, _ptr(Z, f64p),
+                          _ptr(V, u64p))
+    return Z, V
 
 
 # --------------------------------------------------------- single-BDR ops

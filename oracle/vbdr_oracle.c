@@ -368,6 +368,35 @@ void orc_estimate(const orc_pool *p, const uint8_t *M, const uint32_t *hosts,
     free(regs);
 }
 
+/* Estimates straight from a register array M (no pool needed: for pools too
+ * large to hold the oracle's one-DR-per-uint16 state, M comes from
+ * orc_rebuild).  Same steps as orc_estimate. */
+void orc_estimate_M(uint32_t b, uint32_t A0, uint64_t z, const uint8_t *M,
+                    const uint32_t *hosts, uint64_t n, double *out)
+{
+    uint32_t g = 1u << b;
+    double E_tot = orc_hll_raw(M, z);
+    uint8_t *regs = (uint8_t *)malloc(g);
+    for (uint64_t h = 0; h < n; ++h) {
+        for (uint32_t i = 0; i < g; ++i) regs[i] = M[orc_getPhyIdx(hosts[h], i, A0, z)];
+        double E_s = orc_hll_raw(regs, g);
+        out[h] = orc_vhll(z, g, E_s, E_tot);
+    }
+    free(regs);
+}
+
+void orc_host_sums_M(uint32_t b, uint32_t A0, uint64_t z, const uint8_t *M,
+                     const uint32_t *hosts, uint64_t n, double *Z, uint64_t *V)
+{
+    uint32_t g = 1u << b;
+    uint8_t *regs = (uint8_t *)malloc(g);
+    for (uint64_t h = 0; h < n; ++h) {
+        for (uint32_t i = 0; i < g; ++i) regs[i] = M[orc_getPhyIdx(hosts[h], i, A0, z)];
+        orc_hll_sums(regs, g, &Z[h], &V[h]);
+    }
+    free(regs);
+}
+
 /* Per-host harmonic sums (Z_s, V_s) for parity of the integer stage. */
 void orc_host_sums(const orc_pool *p, const uint8_t *M, const uint32_t *hosts,
                    uint64_t n, double *Z, uint64_t *V)

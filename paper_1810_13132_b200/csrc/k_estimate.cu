@@ -11,10 +11,17 @@
 // G lanes cooperate on one host (a "group"); lane `sub` of the group owns the
 // virtual indices i = sub + G q.  s1[i] = H(i, 2^32, A0) (Alg.3) is
 // the same for every host, so the block tabulates it once in shared memory.
-// The gathers are random 1-byte loads from regmax (L2-resident up to 2^26
-// BDRs): the kernel is bound by the SM's L1-to-L2 request rate, one sector
-// per gather; U independent gathers per lane keep
+// The gathers are random 1-byte loads from regmax: L2-resident up to 2^26
+// BDRs, where the kernel is bound by the SM's L1-to-L2 request rate (one
+// sector per gather); U independent gathers per lane keep
 // enough requests in flight.
+//
+// Larger pools (regmax > 64 MiB, e.g. bigwin's 256 MiB) would make every
+// gather a DRAM sector access.  There the kernel runs in passes, each over an
+// L2-sized physical range [p 2^R, (p+1) 2^R): a pass gathers only the indices
+// in its range and adds the packed partial sums S | V << 40 (S <= g 2^L = 2^32)
+// into the 8-byte output slot of the host; the last pass turns the slot into
+// the estimate.  Integer partials make the result independent of the split.
 #include "vbdr_dev.cuh"
 
 using namespace vbdr_dev;
@@ -32,16 +39,17 @@ __device__ __forceinline__ double hll_finish(double agg, double D, double lc, ui
   return E;
 }
 
-template <int G, int U, bool SUMS, bool SMEM>
+template <int G, int U, bool SUMS, bool SMEM, bool MULTI>
 __global__ void __launch_bounds__(kThreads)
 k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *__restrict__ out,
-           unsigned long long *__restrict__ outS, uint32_t *__restrict__ outV) {
+           unsigned long long *__restrict__ outS, uint32_t *__restrict__ outV, uint32_t pass,
+           bool last) {
   extern __shared__ uint32_t s1tab[];
   __shared__ double s_etot_z;  // E_tot / z
   if constexpr (SMEM) {
     for (uint32_t i = threadIdx.x; i < e.g; i += kThreads) s1tab[i] = fmix32(i ^ e.A0);
   }
-  if (!SUMS && threadIdx.x == 0) {
+  if (!SUMS && (!MULTI || last) && threadIdx.x == 0) {
     const unsigned long long St = e.acc[0], Vt = e.acc[1];
     const double D = __dmul_rn((double)St, e.inv2L);  // exact: St <= 2^53
     const double Et = hll_finish(e.azz, D, e.lc_z, Vt, e.z);
@@ -59,7 +67,7 @@ k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *
   for (uint64_t r = 0; warp_first + r < n; r += ngroups) {  // warp-uniform
     const uint64_t h = group + r;
     const bool valid = h < n;
-    const uint32_t aip = valid ? __ldg(hosts + h) : 0u;
+    const uint32_t aip = valid ? (MULTI ? __ldcs(hosts + h) : __ldg(hosts + h)) : 0u;
     unsigned long long S = 0ull;
     uint32_t V = 0u;
     for (uint32_t q = 0; q < per_lane; q += U) {
@@ -68,10 +76,15 @@ k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *
       for (int u = 0; u < U; ++u) {
         const uint32_t i = sub + (uint32_t)G * (q + (uint32_t)u);
         const uint32_t s1 = SMEM ? s1tab[i] : fmix32(i ^ e.A0);
-        M[u] = __ldg(e.regmax + (fmix32(aip ^ s1) & e.mask));
+        const uint32_t pidx = fmix32(aip ^ s1) & e.mask;
+        if constexpr (MULTI)
+          M[u] = (pidx >> e.pass_log2) == pass ? (uint32_t)__ldg(e.regmax + pidx) : 0xFFu;
+        else
+          M[u] = __ldg(e.regmax + pidx);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
+        if (MULTI && M[u] == 0xFFu) continue;  // outside this pass's range
         S += 1ull << (e.L - M[u]);
         V += M[u] == 0u;
       }
@@ -82,6 +95,18 @@ k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *
       V += __shfl_xor_sync(0xffffffffu, V, off);
     }
     if (valid && sub == 0u) {
+      if constexpr (MULTI) {
+        unsigned long long *slot =
+            SUMS ? outS + h : reinterpret_cast<unsigned long long *>(out) + h;
+        unsigned long long packed = S | ((unsigned long long)V << 40);
+        if (pass > 0) packed += __ldcs(slot);
+        if (!last) {
+          __stcs(slot, packed);
+          continue;
+        }
+        S = packed & ((1ull << 40) - 1ull);
+        V = (uint32_t)(packed >> 40);
+      }
       if constexpr (SUMS) {
         outS[h] = S;
         outV[h] = V;
@@ -109,9 +134,29 @@ int sm_count() {
 
 template <int G, int U, bool SMEM>
 cudaError_t run(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
-                unsigned long long *outS, uint32_t *outV, cudaStream_t s) {
+                unsigned long long *outS, uint32_t *outV, cudaStream_t s, uint32_t *nl) {
   const size_t smem = SMEM ? (size_t)e.g * 4 : 0;
-  auto kern = outS ? k_estimate<G, U, true, SMEM> : k_estimate<G, U, false, SMEM>;
+  const uint32_t log2z = 31u - (uint32_t)__builtin_clz((uint32_t)(e.mask)) + 1u;  // mask = z - 1
+  const uint32_t passes = (e.pass_log2 >= log2z) ? 1u : (1u << (log2z - e.pass_log2));
+  *nl = passes;
+  if (passes > 1) {
+    auto kern = outS ? k_estimate<G, U, true, SMEM, true> : k_estimate<G, U, false, SMEM, true>;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess ||
+        per_sm <= 0)
+      per_sm = 1;
+    const uint64_t resident = (uint64_t)per_sm * sm_count();
+    const uint64_t need = (n * G + kThreads - 1) / kThreads;
+    const uint64_t grid = need < resident ? need : resident;
+    for (uint32_t p = 0; p < passes; ++p) {
+      kern<<<(uint32_t)(grid ? grid : 1), kThreads, smem, s>>>(e, hosts, n, out, outS, outV, p,
+                                                              p + 1 == passes);
+      const cudaError_t err = cudaGetLastError();
+      if (err != cudaSuccess) return err;
+    }
+    return cudaSuccess;
+  }
+  auto kern = outS ? k_estimate<G, U, true, SMEM, false> : k_estimate<G, U, false, SMEM, false>;
   // occupancy is cached while the s1 table is too small to limit it (g <= 1024)
   static int per_sm_cache[2] = {0, 0};
   int local = 0;
@@ -123,21 +168,21 @@ cudaError_t run(const EstParams &e, const uint32_t *hosts, uint64_t n, double *o
   const uint64_t resident = (uint64_t)per_sm * sm_count();
   const uint64_t need = (n * G + kThreads - 1) / kThreads;
   const uint64_t grid = need < resident ? need : resident;
-  kern<<<(uint32_t)(grid ? grid : 1), kThreads, smem, s>>>(e, hosts, n, out, outS, outV);
+  kern<<<(uint32_t)(grid ? grid : 1), kThreads, smem, s>>>(e, hosts, n, out, outS, outV, 0u, true);
   return cudaGetLastError();
 }
 
 template <int G>
 cudaError_t run_g(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
-                  unsigned long long *outS, uint32_t *outV, cudaStream_t s) {
+                  unsigned long long *outS, uint32_t *outV, cudaStream_t s, uint32_t *nl) {
   const uint32_t per_lane = e.g / G;
   const bool smem = e.g <= kS1SmemMax;
   if (per_lane >= 8)
-    return smem ? run<G, 8, true>(e, hosts, n, out, outS, outV, s)
-                : run<G, 8, false>(e, hosts, n, out, outS, outV, s);
-  if (per_lane == 4) return run<G, 4, true>(e, hosts, n, out, outS, outV, s);
-  if (per_lane == 2) return run<G, 2, true>(e, hosts, n, out, outS, outV, s);
-  return run<G, 1, true>(e, hosts, n, out, outS, outV, s);
+    return smem ? run<G, 8, true>(e, hosts, n, out, outS, outV, s, nl)
+                : run<G, 8, false>(e, hosts, n, out, outS, outV, s, nl);
+  if (per_lane == 4) return run<G, 4, true>(e, hosts, n, out, outS, outV, s, nl);
+  if (per_lane == 2) return run<G, 2, true>(e, hosts, n, out, outS, outV, s, nl);
+  return run<G, 1, true>(e, hosts, n, out, outS, outV, s, nl);
 }
 
 }  // namespace
@@ -147,18 +192,19 @@ namespace vbdr_launch {
 // Lanes per host: `lanes` if given (a power of two <= min(g, 32)), else 8
 // (best on the caida sweep, profiles/r01_sweep_caida.jsonl), capped at g.
 cudaError_t estimate(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
-                     unsigned long long *outS, uint32_t *outV, cudaStream_t s) {
+                     unsigned long long *outS, uint32_t *outV, cudaStream_t s, uint32_t *nl) {
+  *nl = 0;
   if (n == 0) return cudaSuccess;
   uint32_t G = e.lanes ? e.lanes : 8u;
   if (G > e.g) G = e.g;
   if (G > 32) G = 32;
   switch (G) {
-    case 1: return run_g<1>(e, hosts, n, out, outS, outV, s);
-    case 2: return run_g<2>(e, hosts, n, out, outS, outV, s);
-    case 4: return run_g<4>(e, hosts, n, out, outS, outV, s);
-    case 8: return run_g<8>(e, hosts, n, out, outS, outV, s);
-    case 16: return run_g<16>(e, hosts, n, out, outS, outV, s);
-    case 32: return run_g<32>(e, hosts, n, out, outS, outV, s);
+    case 1: return run_g<1>(e, hosts, n, out, outS, outV, s, nl);
+    case 2: return run_g<2>(e, hosts, n, out, outS, outV, s, nl);
+    case 4: return run_g<4>(e, hosts, n, out, outS, outV, s, nl);
+    case 8: return run_g<8>(e, hosts, n, out, outS, outV, s, nl);
+    case 16: return run_g<16>(e, hosts, n, out, outS, outV, s, nl);
+    case 32: return run_g<32>(e, hosts, n, out, outS, outV, s, nl);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -206,6 +206,18 @@ __global__ void __launch_bounds__(kThreads) k_init(DevParams p, bool fast) {
   }
 }
 
+// ------------------------------------------------------------- export
+// Gather the W packed words of sampled BDRs (parity exports of huge pools).
+__global__ void __launch_bounds__(kThreads)
+k_gather_words(DevParams p, const uint64_t *__restrict__ idx, uint64_t n, uint32_t *out) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const uint64_t j = idx[i];
+    for (uint32_t w = 0; w < p.W; ++w)
+      out[i * p.W + w] = j < p.n_phys ? p.drv[(uint64_t)w * p.n_phys + j] : 0u;
+  }
+}
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -310,6 +322,13 @@ cudaError_t init(const DevParams &p, bool fast, cudaStream_t s) {
 
 cudaError_t slide(const DevParams &p, bool fast, cudaStream_t s) {
   return dispatch_zb<SlideFn>(p.zb, p, fast, s);
+}
+
+cudaError_t gather_words(const DevParams &p, const uint64_t *idx, uint64_t n, uint32_t *out,
+                         cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_gather_words<<<grid_for(k_gather_words, n), kThreads, 0, s>>>(p, idx, n, out);
+  return cudaGetLastError();
 }
 
 cudaError_t scan(const DevParams &p, bool fast, int mode, const uint32_t *pairs, uint64_t n,

@@ -103,12 +103,15 @@ cudaError_t init(const DevParams &p, bool fast, cudaStream_t s);
 cudaError_t scan(const DevParams &p, bool fast, int mode, const uint32_t *pairs, uint64_t n,
                  cudaStream_t s);
 cudaError_t slide(const DevParams &p, bool fast, cudaStream_t s);
+cudaError_t gather_words(const DevParams &p, const uint64_t *idx, uint64_t n, uint32_t *out,
+                         cudaStream_t s);
 
 struct EstParams {
   const uint8_t *regmax;
   const unsigned long long *acc;  // (S_tot, V_tot) of the closed tick
   uint32_t mask, A0, L, g;
   uint32_t lanes;     // lanes per host (0 = default)
+  uint32_t pass_log2; // physical range per pass = 2^pass_log2 BDRs (>= log2(n_phys): one pass)
   double inv2L;       // 2^-L
   double agg;         // alpha_g * g * g
   double lc_g;        // 2.5 * g
@@ -117,6 +120,7 @@ struct EstParams {
   double z;           // n_phys as double
   double C;           // z g / (z - g)
 };
+// *nl receives the number of kernels launched (passes).
 cudaError_t estimate(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
-                     unsigned long long *outS, uint32_t *outV, cudaStream_t s);
+                     unsigned long long *outS, uint32_t *outV, cudaStream_t s, uint32_t *nl);
 }  // namespace vbdr_launch

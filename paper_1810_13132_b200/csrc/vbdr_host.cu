@@ -66,6 +66,7 @@ std::string plan(const vbdr_config *c, vbdr_config *norm, Plan *pl) {
   if (n.scan_mode > 4) return "scan_mode must be 0..4";
   if (n.est_lanes > 32 || (n.est_lanes & (n.est_lanes - 1)))
     return "est_lanes must be 0 or a power of two <= 32";
+  if (n.est_pass_log2 > 32) return "est_pass_log2 must be 0..32";
   if (n.m < 2 || !is_pow2(n.m)) return "m must be a power of two >= 2";
   if (n.k < 1) return "k must be >= 1";
   if (n.n_phys < 4 || !is_pow2(n.n_phys) || n.n_phys > (1ull << 32))
@@ -146,6 +147,11 @@ vbdr_launch::EstParams est_params(const vbdr *h) {
   e.L = h->p.L;
   e.g = h->cfg.m;
   e.lanes = h->cfg.est_lanes;
+  // passes over L2-sized physical ranges (k_estimate.cu); 2^26 one-byte
+  // registers = 64 MiB stays L2-resident on B200 (126 MB L2).  The packed
+  // partial sums need g < 2^24.
+  e.pass_log2 = h->cfg.est_pass_log2 ? h->cfg.est_pass_log2 : 26u;
+  if (h->cfg.m >= (1u << 24)) e.pass_log2 = 32;
   e.inv2L = std::ldexp(1.0, -(int)h->p.L);
   const double g = (double)h->cfg.m, z = (double)h->cfg.n_phys;
   e.agg = h->alpha_g * g * g;  // exact: g is a power of two
@@ -155,6 +161,24 @@ vbdr_launch::EstParams est_params(const vbdr *h) {
   e.z = z;
   e.C = ((double)h->cfg.n_phys * (double)h->cfg.m) / (double)(h->cfg.n_phys - h->cfg.m);
   return e;
+}
+
+// Unpack one BDR's DR ages from its W packed words (word(w) accessor).
+// mode 0: stored values; mode 1: canonical C_k = min(age, k) at the last
+// boundary (layout P stores ages already advanced by Alg.8: undo it).
+template <typename WordAt>
+void decode_ages(const vbdr *h, WordAt word, int mode, uint16_t *out) {
+  const uint32_t F = h->p.F, zb = h->p.zb, L = h->p.L, k = h->p.k;
+  const uint32_t fm = (1u << zb) - 1u, sent = fm;
+  for (uint32_t r = 1; r <= L; ++r) {
+    const uint32_t w = (r - 1) / F, f = (r - 1) % F;
+    uint32_t v = (word(w) >> (zb * f)) & fm;
+    if (mode == 1) {
+      if (!h->fast) v = (v == sent) ? k : (v ? v - 1u : 0u);
+      if (v > k) v = k;
+    }
+    out[r - 1] = (uint16_t)v;
+  }
 }
 
 vbdr_status ensure_pipeline(vbdr *h) {
@@ -314,10 +338,11 @@ vbdr_status vbdr_estimate(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, 
   if (n_hosts == 0) return VBDR_OK;
   if (!d_hosts || !d_out) return fail(h, VBDR_EINVAL, "null d_hosts/d_out");
   if (vbdr_status s = check_async(h, "before estimate")) return s;
-  const cudaError_t e =
-      vbdr_launch::estimate(est_params(h), d_hosts, n_hosts, d_out, nullptr, nullptr, S(stream));
+  uint32_t nl = 0;
+  const cudaError_t e = vbdr_launch::estimate(est_params(h), d_hosts, n_hosts, d_out, nullptr,
+                                              nullptr, S(stream), &nl);
   if (e != cudaSuccess) return cuda_fail(h, e, "estimate launch");
-  h->info.launches += 1;
+  h->info.launches += nl;
   return VBDR_OK;
 }
 
@@ -327,11 +352,12 @@ vbdr_status vbdr_host_sums(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
   if (n_hosts == 0) return VBDR_OK;
   if (!d_hosts || !d_S || !d_V) return fail(h, VBDR_EINVAL, "null pointer");
   if (vbdr_status s = check_async(h, "before host_sums")) return s;
+  uint32_t nl = 0;
   const cudaError_t e = vbdr_launch::estimate(est_params(h), d_hosts, n_hosts, nullptr,
                                               reinterpret_cast<unsigned long long *>(d_S), d_V,
-                                              S(stream));
+                                              S(stream), &nl);
   if (e != cudaSuccess) return cuda_fail(h, e, "host_sums launch");
-  h->info.launches += 1;
+  h->info.launches += nl;
   return VBDR_OK;
 }
 
@@ -383,11 +409,12 @@ vbdr_status vbdr_estimate_host(vbdr_t *h, const uint32_t *h_hosts, uint64_t n_ho
   cudaStream_t cs = S(stream);
   cudaError_t e =
       cudaMemcpyAsync(d_hosts_stage, h_hosts, 4ull * n_hosts, cudaMemcpyHostToDevice, cs);
+  uint32_t nl = 0;
   if (e == cudaSuccess)
     e = vbdr_launch::estimate(est_params(h), d_hosts_stage, n_hosts, d_out_stage, nullptr,
-                              nullptr, cs);
+                              nullptr, cs, &nl);
   if (e == cudaSuccess) {
-    h->info.launches += 1;
+    h->info.launches += nl;
     e = cudaMemcpyAsync(h_out, d_out_stage, 8ull * n_hosts, cudaMemcpyDeviceToHost, cs);
   }
   if (e != cudaSuccess) return cuda_fail(h, e, "estimate_host");
@@ -397,7 +424,7 @@ vbdr_status vbdr_estimate_host(vbdr_t *h, const uint32_t *h_hosts, uint64_t n_ho
 vbdr_status vbdr_export_ages(vbdr_t *h, uint16_t *h_ages, int mode, void *stream) {
   if (!h || !h_ages || (mode != 0 && mode != 1)) return VBDR_EINVAL;
   const uint64_t n = h->p.n_phys;
-  const uint32_t W = h->p.W, F = h->p.F, zb = h->p.zb, L = h->p.L, k = h->p.k;
+  const uint32_t W = h->p.W;
   std::vector<uint32_t> words;
   try {
     words.resize((size_t)(W * n));
@@ -408,18 +435,34 @@ vbdr_status vbdr_export_ages(vbdr_t *h, uint16_t *h_ages, int mode, void *stream
   cudaError_t e = cudaMemcpyAsync(words.data(), h->p.drv, 4ull * W * n, cudaMemcpyDeviceToHost, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e != cudaSuccess) return cuda_fail(h, e, "export_ages");
-  const uint32_t fm = (1u << zb) - 1u, sent = fm;
-  for (uint64_t j = 0; j < n; ++j) {
-    for (uint32_t r = 1; r <= L; ++r) {
-      const uint32_t w = (r - 1) / F, f = (r - 1) % F;
-      uint32_t v = (words[(size_t)(w * n + j)] >> (zb * f)) & fm;
-      if (mode == 1) {
-        if (!h->fast) v = (v == sent) ? k : (v ? v - 1u : 0u);  // undo the hoisted Alg.8 ageing
-        if (v > k) v = k;
-      }
-      h_ages[j * L + (r - 1)] = (uint16_t)v;
-    }
+  for (uint64_t j = 0; j < n; ++j)
+    decode_ages(h, [&](uint32_t w) { return words[(size_t)(w * n + j)]; }, mode,
+                h_ages + j * h->p.L);
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_export_ages_at(vbdr_t *h, const uint64_t *d_idx, uint64_t n_idx,
+                                uint32_t *d_scratch, uint16_t *h_ages, int mode, void *stream) {
+  if (!h || (n_idx && (!d_idx || !d_scratch || !h_ages)) || (mode != 0 && mode != 1))
+    return VBDR_EINVAL;
+  if (n_idx == 0) return VBDR_OK;
+  const uint32_t W = h->p.W;
+  std::vector<uint32_t> words;
+  try {
+    words.resize((size_t)(W * n_idx));
+  } catch (...) {
+    return fail(h, VBDR_ENOMEM, "host buffer");
   }
+  cudaStream_t cs = S(stream);
+  cudaError_t e = vbdr_launch::gather_words(h->p, d_idx, n_idx, d_scratch, cs);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(words.data(), d_scratch, 4ull * W * n_idx, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return cuda_fail(h, e, "export_ages_at");
+  h->info.launches += 1;
+  for (uint64_t i = 0; i < n_idx; ++i)
+    decode_ages(h, [&](uint32_t w) { return words[(size_t)(i * W + w)]; }, mode,
+                h_ages + i * h->p.L);
   return VBDR_OK;
 }
 

@@ -26,7 +26,7 @@ class vbdr_config(C.Structure):
     _fields_ = [("m", C.c_uint32), ("k", C.c_uint32), ("n_phys", C.c_uint64),
                 ("seed_a0", C.c_uint32), ("seed_a1", C.c_uint32), ("zbits", C.c_uint32),
                 ("rank_cap", C.c_uint32), ("layout", C.c_uint32), ("scan_mode", C.c_uint32),
-                ("est_lanes", C.c_uint32)]
+                ("est_lanes", C.c_uint32), ("est_pass_log2", C.c_uint32)]
 
 
 class vbdr_info_t(C.Structure):
@@ -40,7 +40,8 @@ class vbdr_info_t(C.Structure):
 # Every symbol include/vbdr.h declares (tests check the library exports them).
 SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice", "vbdr_slide",
            "vbdr_estimate", "vbdr_host_sums", "vbdr_scan_slice_host", "vbdr_estimate_host",
-           "vbdr_info", "vbdr_export_ages", "vbdr_export_regmax", "vbdr_export_pool_sums",
+           "vbdr_info", "vbdr_export_ages", "vbdr_export_ages_at", "vbdr_export_regmax",
+           "vbdr_export_pool_sums",
            "vbdr_last_error", "vbdr_status_string")
 
 _lib = None
@@ -67,6 +68,7 @@ def lib():
             "vbdr_estimate_host": [vp, vp, u64, vp, vp, vp, vp],
             "vbdr_info": [vp, C.POINTER(vbdr_info_t)],
             "vbdr_export_ages": [vp, vp, C.c_int, vp],
+            "vbdr_export_ages_at": [vp, vp, u64, vp, vp, C.c_int, vp],
             "vbdr_export_regmax": [vp, vp, vp],
             "vbdr_export_pool_sums": [vp, C.POINTER(u64), C.POINTER(u64), vp],
         }
@@ -85,9 +87,10 @@ def lib():
 def make_config(m: int, k: int, n_phys: int, seed_a0: int = 0x5EED0001,
                 seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
                 layout: str | int = "fast", scan_mode: int = 0,
-                est_lanes: int = 0) -> vbdr_config:
+                est_lanes: int = 0, est_pass_log2: int = 0) -> vbdr_config:
     lay = LAYOUTS[layout] if isinstance(layout, str) else int(layout)
-    return vbdr_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, lay, scan_mode, est_lanes)
+    return vbdr_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, lay, scan_mode, est_lanes,
+                       est_pass_log2)
 
 
 def state_bytes(cfg: vbdr_config) -> int:
@@ -110,14 +113,14 @@ class VBDR:
 
     def __init__(self, m: int, k: int, n_phys: int, *, seed_a0: int = 0x5EED0001,
                  seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
-                 layout: str = "fast", scan_mode: int = 0, est_lanes: int = 0, device=None,
-                 stream=None):
+                 layout: str = "fast", scan_mode: int = 0, est_lanes: int = 0,
+                 est_pass_log2: int = 0, device=None, stream=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("VBDR needs a CUDA device (no CPU fallback)")
         self.device = torch.device(device if device is not None else "cuda")
         self.cfg = make_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, layout, scan_mode,
-                               est_lanes)
+                               est_lanes, est_pass_log2)
         nbytes = state_bytes(self.cfg)
         with torch.cuda.device(self.device):
             self.state = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -226,6 +229,21 @@ class VBDR:
                                            1 if canonical else 0, _stream_ptr(stream)),
                     "vbdr_export_ages")
         return out.reshape(self.n_phys, L)
+
+    def export_ages_at(self, idx, canonical: bool = False, stream=None):
+        """``vbdr_export_ages_at``: ages of the sampled BDRs ``idx`` (numpy int)."""
+        import numpy as np
+        import torch
+        inf = self.info()
+        d_idx = torch.from_numpy(np.ascontiguousarray(idx, dtype=np.int64)).to(self.device)
+        scratch = torch.empty(len(idx) * inf["words"], dtype=torch.int32, device=self.device)
+        out = np.empty(len(idx) * inf["L"], dtype=np.uint16)
+        self._check(lib().vbdr_export_ages_at(self._h, C.c_void_p(d_idx.data_ptr()), len(idx),
+                                              C.c_void_p(scratch.data_ptr()),
+                                              out.ctypes.data_as(C.c_void_p),
+                                              1 if canonical else 0, _stream_ptr(stream)),
+                    "vbdr_export_ages_at")
+        return out.reshape(len(idx), inf["L"])
 
     def export_regmax(self, stream=None):
         import numpy as np

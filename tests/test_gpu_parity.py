@@ -81,8 +81,9 @@ def compare_boundary(pool, ref: oracle.Pool, refs_other, hosts_np, hosts_dev, wi
 
 
 @pytest.mark.parametrize("layout", ["fast", "packed"])
-@pytest.mark.parametrize("scan_mode,est_lanes", [(1, 0), (2, 1), (4, 8), (1, 32), (4, 2)])
-def test_tiny_every_boundary(layout, scan_mode, est_lanes):
+@pytest.mark.parametrize("scan_mode,est_lanes,passes", [(1, 0, 0), (2, 1, 0), (4, 8, 10), (1, 32, 0),
+                                                       (4, 2, 7), (0, 0, 11)])
+def test_tiny_every_boundary(layout, scan_mode, est_lanes, passes):
     """configs[0] 'tiny': 10k pairs/slice, 64 hosts, m=32, 2^12 BDRs, k=4."""
     tr = synth.CONFIGS["tiny"]
     cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
@@ -90,7 +91,7 @@ def test_tiny_every_boundary(layout, scan_mode, est_lanes):
     ref = oracle.Pool(cfg, variant)
     others = [oracle.Pool(cfg, v) for v in ("gfast", "gsmall" if layout == "fast" else "serial")]
     pool = VBDR(32, 4, 1 << 12, layout=layout, scan_mode=scan_mode, est_lanes=est_lanes,
-                device=DEV)
+                est_pass_log2=passes, device=DEV)
     hosts_np = tr.host_ids()
     hosts = dev_u32(hosts_np)
     slices = []
@@ -222,8 +223,8 @@ def test_synth_cuda_twin_matches_numpy():
             assert np.array_equal(got, synth.generate(tr, t, start, count))
 
 
-@pytest.mark.parametrize("layout", ["fast", "packed"])
-def test_caida_full_size(layout):
+@pytest.mark.parametrize("layout,pass_log2", [("fast", 0), ("packed", 0), ("fast", 20)])
+def test_caida_full_size(layout, pass_log2):
     """configs[1] 'caida' at full size (5M pairs/slice, 2^22 BDRs, m=128, k=5,
     500k hosts) in the launch configuration bench.py times: every register,
     the pool sums and all 500k host sums bit-exact, all estimates to 1e-9,
@@ -231,7 +232,7 @@ def test_caida_full_size(layout):
     tr = synth.CONFIGS["caida"]
     cfg = oracle.PoolConfig(b=7, k=5, z=1 << 22)
     ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
-    pool = VBDR(128, 5, 1 << 22, layout=layout, device=DEV)
+    pool = VBDR(128, 5, 1 << 22, layout=layout, est_pass_log2=pass_log2, device=DEV)
     hosts_np = tr.host_ids()
     hosts = dev_u32(hosts_np)
     rng = np.random.default_rng(5)

@@ -159,3 +159,17 @@ def test_exact_cardinality_definition():
     s1 = np.array([[1, 9], [1, 10], [2, 9]], dtype=np.uint32)
     assert oracle.exact_cardinality([s1], 1) == 2
     assert oracle.exact_cardinalities([s0, s1]) == {1: 2, 2: 1}
+
+
+def test_estimate_from_register_array_matches_pool():
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    tr = synth.CONFIGS["tiny"]
+    p = oracle.Pool(cfg, "serial")
+    for t in range(5):
+        p.slice(synth.generate(tr, t))
+    M = p.readout()
+    hosts = tr.host_ids()
+    assert np.array_equal(oracle.estimate_M(M, hosts, cfg.b, cfg.z), p.estimate(M, hosts))
+    Z, V = oracle.host_sums_M(M, hosts, cfg.b, cfg.z)
+    Z2, V2 = p.host_sums(M, hosts)
+    assert np.array_equal(Z, Z2) and np.array_equal(V, V2)
