@@ -159,9 +159,12 @@ vbdr_status vbdr_host_sums(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
 
 /* vbdr_scan_slice on HOST pairs: copies h_pairs (pinned for overlap) through
  * the caller's device staging buffer d_stage (u32[2*stage_pairs], split in
- * two halves) chunk by chunk, overlapping each chunk's host-to-device copy
- * with the scan of the previous chunk.  Stream-ordered on `stream`; h_pairs
- * must stay valid until that stream reaches this point. */
+ * two halves) chunk by chunk on an internal copy stream, overlapping each
+ * chunk's host-to-device copy with the scan of the previous chunk -- and,
+ * across calls, with the slide/estimate queued in between (a copy into a half
+ * waits only for the last scan that read it).  Scans are ordered on `stream`;
+ * h_pairs must stay valid until `stream` reaches this point.  Use the same
+ * staging buffer for consecutive calls. */
 vbdr_status vbdr_scan_slice_host(vbdr_t *h, const uint32_t *h_pairs, uint64_t n_pairs,
                                  uint32_t *d_stage, uint64_t stage_pairs, void *stream);
 

@@ -181,12 +181,14 @@ void decode_ages(const vbdr *h, WordAt word, int mode, uint16_t *out) {
   }
 }
 
-vbdr_status ensure_pipeline(vbdr *h) {
+vbdr_status ensure_pipeline(vbdr *h, cudaStream_t cs) {
   if (h->copy_stream) return VBDR_OK;
   cudaError_t e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
     e = cudaEventCreateWithFlags(&h->ev_copied[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_scanned[i], cudaEventDisableTiming);
+    // "slot i is free" starts out as: everything queued on the caller's stream so far
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_scanned[i], cs);
   }
   if (e != cudaSuccess) return cuda_fail(h, e, "pipeline resources");
   return VBDR_OK;
@@ -368,14 +370,16 @@ vbdr_status vbdr_scan_slice_host(vbdr_t *h, const uint32_t *h_pairs, uint64_t n_
   if (!h_pairs || !d_stage || stage_pairs < 16 ||
       (reinterpret_cast<uintptr_t>(d_stage) & 15u))
     return fail(h, VBDR_EINVAL, "bad host pairs / staging buffer");
-  if (vbdr_status s = ensure_pipeline(h)) return s;
-  if (vbdr_status s = check_async(h, "before scan_host")) return s;
   cudaStream_t cs = S(stream);
+  if (vbdr_status s = ensure_pipeline(h, cs)) return s;
+  if (vbdr_status s = check_async(h, "before scan_host")) return s;
   // two halves of the staging buffer, each a multiple of 2 pairs (16 B)
   const uint64_t half = (stage_pairs / 2) & ~uint64_t(1);
-  // the copy stream must not overtake work already queued on `stream`
-  cudaError_t e = cudaEventRecord(h->ev_scanned[0], cs);
-  if (e == cudaSuccess) e = cudaEventRecord(h->ev_scanned[1], cs);
+  // A copy into a half waits only for the last scan that read that half
+  // (ev_scanned, carried across calls): the host-to-device copies of the next
+  // slice overlap this slice's slide and estimate.  Each chunk's scan waits
+  // for its copy.
+  cudaError_t e = cudaSuccess;
   uint64_t done = 0;
   for (uint64_t c = 0; done < n_pairs && e == cudaSuccess; ++c) {
     const int slot = (int)(c & 1u);
