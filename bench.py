@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--layout", default="fast", choices=["fast", "packed"])
     ap.add_argument("--scan-mode", type=int, default=0)
     ap.add_argument("--est-lanes", type=int, default=0)
+    ap.add_argument("--merge", default="sharded", choices=["stamps", "delta", "sharded"],
+                    help="N>1 slide merge (paper_1810_13132_b200.slide_merged)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -248,7 +250,8 @@ def run_vbdr(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1810_13132_b200 import VBDR, merge_stamps, shard_range
+    from paper_1810_13132_b200 import (VBDR, all_gather_shards, merge_stamps, reduce_scatter_max,
+                                       shard_range)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -264,6 +267,8 @@ def run_vbdr(args):
 
     tr = synth.CONFIGS[args.config]
     wl = WORKLOADS[args.config]
+    if world > 1 and args.layout != "fast":
+        raise SystemExit("multi-GPU needs --layout fast (NCCL has no bitwise-AND merge for packed)")
     pool = VBDR(wl["m"], wl["k"], wl["n_phys"], layout=args.layout, scan_mode=args.scan_mode,
                 est_lanes=args.est_lanes, device=dev)
     info = pool.info()
@@ -291,23 +296,50 @@ def run_vbdr(args):
 
     E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    n_shard = wl["n_phys"] // world
+    delta_buf = torch.empty(wl["n_phys"], dtype=torch.uint8, device=dev) if world > 1 else None
+    shard_buf = torch.empty(n_shard, dtype=torch.uint8, device=dev) if world > 1 else None
+
+    def mark(evs, j):
+        if evs:
+            evs[j].record(stream)
+
+    def close_slice(evs=None):
+        """slide_merged, spelled out so each phase gets its own events:
+        [merge] -> slide kernel -> [register all-gather + pool-sum all-reduce]."""
+        if world == 1:
+            mark(evs, 2)
+            pool.slide()
+            mark(evs, 3)
+        elif args.merge == "stamps":
+            merge_stamps(pool, group)
+            mark(evs, 2)
+            pool.slide()
+            mark(evs, 3)
+        elif args.merge == "delta":
+            pool.stamp_delta(delta_buf)
+            dist.all_reduce(delta_buf, op=dist.ReduceOp.MAX, group=group)
+            mark(evs, 2)
+            pool.slide_delta(delta_buf)
+            mark(evs, 3)
+        else:
+            pool.stamp_delta(delta_buf)
+            reduce_scatter_max(delta_buf, shard_buf, group)
+            mark(evs, 2)
+            pool.slide_delta(shard_buf, rank * n_shard, (rank + 1) * n_shard)
+            mark(evs, 3)
+            all_gather_shards(pool.regmax_view(), group)
+            dist.all_reduce(pool.acc_view(), op=dist.ReduceOp.SUM, group=group)
+        mark(evs, 4)
+
     def step(i, evs=None):
         x = inputs[i % n_inputs]
-        if evs:
-            evs[0].record(stream)
+        mark(evs, 0)
         pool.scan_slice(x)
-        if evs:
-            evs[1].record(stream)
-        if group is not None:
-            merge_stamps(pool, group)
-        if evs:
-            evs[2].record(stream)
-        pool.slide()
-        if evs:
-            evs[3].record(stream)
+        mark(evs, 1)
+        close_slice(evs)
         pool.estimate(hosts, out=est_out)
-        if evs:
-            evs[4].record(stream)
+        mark(evs, 5)
 
     # warm-up
     for i in range(args.warmup):
@@ -317,7 +349,7 @@ def run_vbdr(args):
 
     # ---- device-resident timed region
     clocks = ClockSampler(local) if rank == 0 else None
-    events = [[E() for _ in range(5)] for _ in range(args.steps)]
+    events = [[E() for _ in range(6)] for _ in range(args.steps)]
     launches0 = pool.info()["launches"]
     barrier()
     for i in range(args.steps):
@@ -326,10 +358,11 @@ def run_vbdr(args):
     barrier()
     launches = pool.info()["launches"] - launches0
     clk = clocks.stop() if clocks else None
-    ms = np.array([[ev[j].elapsed_time(ev[j + 1]) for j in range(4)] for ev in events])
+    ms = np.array([[ev[j].elapsed_time(ev[j + 1]) for j in range(5)] for ev in events])
     step_ms_local = ms.sum(axis=1)
     local_total = float(step_ms_local.sum())
-    per_kernel_local = ms.mean(axis=0)  # scan, merge, slide, estimate
+    ms_k = ms.mean(axis=0)  # scan, merge, slide, gather, estimate
+    per_kernel_local = np.array([ms_k[0], ms_k[1] + ms_k[3], ms_k[2], ms_k[4]])
     if world > 1:
         t = torch.tensor([local_total, *per_kernel_local.tolist()], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -353,9 +386,7 @@ def run_vbdr(args):
 
         def e2e_step(i):
             pool.scan_slice_host(h_inputs[i % len(h_inputs)], stage)
-            if group is not None:
-                merge_stamps(pool, group)
-            pool.slide()
+            close_slice()
             pool.estimate_host(h_hosts, hstage, ostage, h_out)
 
         for i in range(3):
@@ -436,7 +467,8 @@ def run_vbdr(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": args.config, "layout": args.layout, **wl,
                    "pairs_per_slice": tr.pairs_per_slice, "hosts": tr.hosts,
-                   "parallelism": f"pairs+hosts sharded x{world}, allreduce(MAX) merge",
+                   "parallelism": (f"pairs+hosts sharded x{world}, merge={args.merge}"
+                                   if world > 1 else "single GPU"),
                    "l2": f"flushed before every step ({args.flush_mib} MiB write)",
                    "scan_mode": args.scan_mode, "est_lanes": args.est_lanes,
                    "zbits": info["zbits"], "words_per_bdr": info["words"],

@@ -141,6 +141,25 @@ vbdr_status vbdr_scan_slice(vbdr_t *h, const uint32_t *d_pairs, uint64_t n_pairs
  * max over sr, see vbdr_info) BEFORE this call. */
 vbdr_status vbdr_slide(vbdr_t *h, void *stream);
 
+/* ---- multi-GPU merge (layout fast) ----------------------------------- */
+
+/* Compact the open slice's stamps to one byte per BDR (d_delta, u8[n_phys],
+ * 16-byte aligned): the slice's max rank rho at BDR j, or 0 -- the paper's
+ * nowLBP1.  The elementwise MAX of the ranks' deltas
+ * (NCCL allreduce / reduce-scatter on uint8) is the whole slice's nowLBP1,
+ * because max is commutative and idempotent.  VBDR_ESTATE on layout packed. */
+vbdr_status vbdr_stamp_delta(vbdr_t *h, uint8_t *d_delta, void *stream);
+
+/* vbdr_slide driven by a MERGED delta instead of the local stamps, over the
+ * BDR range [j0, j1) only (multiples of 4; d_delta[j - j0] is BDR j's rank).
+ * With [0, n_phys) every rank slides its full replica; with a shard per rank
+ * the ranks then all-gather regmax (vbdr_info off_regmax) and all-reduce (SUM)
+ * the pool sums of the closed tick (the two u64 at off_acc + 16 * (T & 1),
+ * T = the closed tick) before estimating.  DRs outside [j0, j1) are not aged
+ * and must not be used afterwards.  Closes the slice like vbdr_slide. */
+vbdr_status vbdr_slide_delta(vbdr_t *h, const uint8_t *d_delta, uint64_t j0, uint64_t j1,
+                             void *stream);
+
 /* Estimate |OP(aip, t, k)| (Definition 1) for n_hosts hosts
  * over the window W(t-k+1..t) of the last closed slice: Alg.5 gather
  * (PAPER.md:197-213), HyperLogLog harmonic mean with linear counting, vHLL

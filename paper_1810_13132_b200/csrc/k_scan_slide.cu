@@ -97,9 +97,13 @@ k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict
 //   PACKED: M = GetLBP1BDR of the ages at this boundary (Alg.2), then age all
 //           DRs for the next slice (Alg.8 hoisted from the next slice open).
 // Writes regmax[j] = M and accumulates S_tot = sum 2^(L-M), V_tot = #{M=0}.
-template <bool FAST, int ZB>
+// Multi-GPU: DELTA = true reads this slice's max ranks from a merged u8
+// array (delta4[q - q0] packs BDRs 4q..4q+3) instead of the local stamps, and
+// only BDR quads [q0, q1) are processed (the rank's shard).
+template <bool FAST, int ZB, bool DELTA>
 __global__ void __launch_bounds__(kThreads)
-k_slide(DevParams p, uint32_t addk, uint32_t slot) {
+k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ delta4,
+        uint64_t q0, uint64_t q1) {
   using S = Swar<ZB>;
   constexpr int WM = WMax<ZB>::value;
   const uint64_t n4 = p.n_phys >> 2;
@@ -109,9 +113,13 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot) {
   unsigned long long s_acc = 0;
   uint32_t v_acc = 0;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  for (uint64_t q = (uint64_t)blockIdx.x * kThreads + threadIdx.x; q < n4; q += stride) {
-    uint32_t hit[4] = {0u, 0u, 0u, 0u};  // 1 + rank-1 of this slice's max rank, or 0
-    if constexpr (FAST) {
+  for (uint64_t q = q0 + (uint64_t)blockIdx.x * kThreads + threadIdx.x; q < q1; q += stride) {
+    uint32_t hit[4] = {0u, 0u, 0u, 0u};  // this slice's max rank of each BDR, or 0
+    if constexpr (FAST && DELTA) {
+      const uint32_t d = __ldcs(delta4 + (q - q0));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) hit[c] = (d >> (8 * c)) & 0xFFu;
+    } else if constexpr (FAST) {
       const uint4 s = __ldcs(sr4 + q);
       const uint32_t sv[4] = {s.x, s.y, s.z, s.w};
 #pragma unroll
@@ -180,6 +188,23 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot) {
       p.acc[2 * (slot ^ 1u)] = 0ull;
       p.acc[2 * (slot ^ 1u) + 1] = 0ull;
     }
+  }
+}
+
+// ------------------------------------------------------------- delta
+// Compact the stamps of the open slice to one byte per BDR: rho if the stamp
+// is from tick T, else 0 (the u8 merge payload, 4x less than the stamps).
+__global__ void __launch_bounds__(kThreads) k_delta(DevParams p, uint32_t *__restrict__ delta4) {
+  const uint64_t n4 = p.n_phys >> 2;
+  const uint4 *sr4 = reinterpret_cast<const uint4 *>(p.sr);
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t q = (uint64_t)blockIdx.x * kThreads + threadIdx.x; q < n4; q += stride) {
+    const uint4 s = __ldcs(sr4 + q);
+    const uint32_t sv[4] = {s.x, s.y, s.z, s.w};
+    uint32_t d = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) d |= (((sv[c] >> 5) == p.tick) ? (sv[c] & 31u) : 0u) << (8 * c);
+    __stcs(delta4 + q, d);
   }
 }
 
@@ -273,16 +298,22 @@ struct InitFn {
 
 template <int ZB>
 struct SlideFn {
-  static cudaError_t run(const DevParams &p, bool fast, cudaStream_t s) {
+  static cudaError_t run(const DevParams &p, bool fast, const uint32_t *delta4, uint64_t q0,
+                         uint64_t q1, cudaStream_t s) {
     // (2^zb - k) at every even field's LSB (Swar::active)
     uint32_t addk = 0;
     for (uint32_t f = 0; f < Swar<ZB>::F; f += 2) addk |= ((1u << ZB) - p.k) << (ZB * f);
     const uint32_t slot = p.tick & 1u;
-    const uint64_t work = p.n_phys >> 2;
-    if (fast)
-      k_slide<true, ZB><<<grid_for(k_slide<true, ZB>, work), kThreads, 0, s>>>(p, addk, slot);
+    const uint64_t work = q1 - q0;
+    if (fast && delta4)
+      k_slide<true, ZB, true><<<grid_for(k_slide<true, ZB, true>, work), kThreads, 0, s>>>(
+          p, addk, slot, delta4, q0, q1);
+    else if (fast)
+      k_slide<true, ZB, false><<<grid_for(k_slide<true, ZB, false>, work), kThreads, 0, s>>>(
+          p, addk, slot, nullptr, q0, q1);
     else
-      k_slide<false, ZB><<<grid_for(k_slide<false, ZB>, work), kThreads, 0, s>>>(p, addk, slot);
+      k_slide<false, ZB, false><<<grid_for(k_slide<false, ZB, false>, work), kThreads, 0, s>>>(
+          p, addk, slot, nullptr, q0, q1);
     return cudaGetLastError();
   }
 };
@@ -321,7 +352,19 @@ cudaError_t init(const DevParams &p, bool fast, cudaStream_t s) {
 }
 
 cudaError_t slide(const DevParams &p, bool fast, cudaStream_t s) {
-  return dispatch_zb<SlideFn>(p.zb, p, fast, s);
+  return dispatch_zb<SlideFn>(p.zb, p, fast, (const uint32_t *)nullptr, (uint64_t)0,
+                              p.n_phys >> 2, s);
+}
+
+cudaError_t slide_delta(const DevParams &p, const uint8_t *delta, uint64_t j0, uint64_t j1,
+                        cudaStream_t s) {
+  return dispatch_zb<SlideFn>(p.zb, p, true, reinterpret_cast<const uint32_t *>(delta), j0 >> 2,
+                              j1 >> 2, s);
+}
+
+cudaError_t delta(const DevParams &p, uint8_t *out, cudaStream_t s) {
+  k_delta<<<grid_for(k_delta, p.n_phys >> 2), kThreads, 0, s>>>(p, reinterpret_cast<uint32_t *>(out));
+  return cudaGetLastError();
 }
 
 cudaError_t gather_words(const DevParams &p, const uint64_t *idx, uint64_t n, uint32_t *out,

@@ -103,6 +103,9 @@ cudaError_t init(const DevParams &p, bool fast, cudaStream_t s);
 cudaError_t scan(const DevParams &p, bool fast, int mode, const uint32_t *pairs, uint64_t n,
                  cudaStream_t s);
 cudaError_t slide(const DevParams &p, bool fast, cudaStream_t s);
+cudaError_t slide_delta(const DevParams &p, const uint8_t *delta, uint64_t j0, uint64_t j1,
+                        cudaStream_t s);
+cudaError_t delta(const DevParams &p, uint8_t *out, cudaStream_t s);
 cudaError_t gather_words(const DevParams &p, const uint64_t *idx, uint64_t n, uint32_t *out,
                          cudaStream_t s);
 

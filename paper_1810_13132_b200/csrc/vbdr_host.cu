@@ -194,6 +194,23 @@ vbdr_status ensure_pipeline(vbdr *h, cudaStream_t cs) {
   return VBDR_OK;
 }
 
+// Advance the host-side slice clock after a slide (shared by the slide paths).
+vbdr_status after_slide(vbdr_t *h, void *stream) {
+  h->info.launches += 1;
+  h->info.slices_closed += 1;
+  h->p.tick += 1;
+  if (h->p.tick >= kTickLimit) {
+    // Every stamp is stale after a slide; restart the tick at 2 (same parity
+    // as kTickLimit, so the accumulator slots keep alternating).
+    if (h->fast) {
+      const cudaError_t m = cudaMemsetAsync(h->p.sr, 0, 4ull * h->p.n_phys, S(stream));
+      if (m != cudaSuccess) return cuda_fail(h, m, "tick wrap");
+    }
+    h->p.tick = 2;
+  }
+  return VBDR_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -319,19 +336,32 @@ vbdr_status vbdr_slide(vbdr_t *h, void *stream) {
   if (vbdr_status s = check_async(h, "before slide")) return s;
   const cudaError_t e = vbdr_launch::slide(h->p, h->fast, S(stream));
   if (e != cudaSuccess) return cuda_fail(h, e, "slide launch");
+  return after_slide(h, stream);
+}
+
+vbdr_status vbdr_stamp_delta(vbdr_t *h, uint8_t *d_delta, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (!h->fast) return fail(h, VBDR_ESTATE, "stamp deltas exist only in layout fast");
+  if (!d_delta || (reinterpret_cast<uintptr_t>(d_delta) & 15u))
+    return fail(h, VBDR_EINVAL, "d_delta must be a 16-byte aligned device pointer");
+  if (vbdr_status s = check_async(h, "before stamp_delta")) return s;
+  const cudaError_t e = vbdr_launch::delta(h->p, d_delta, S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "stamp_delta launch");
   h->info.launches += 1;
-  h->info.slices_closed += 1;
-  h->p.tick += 1;
-  if (h->p.tick >= kTickLimit) {
-    // Every stamp is stale after a slide; restart the tick at 2 (same parity
-    // as kTickLimit, so the accumulator slots keep alternating).
-    if (h->fast) {
-      const cudaError_t m = cudaMemsetAsync(h->p.sr, 0, 4ull * h->p.n_phys, S(stream));
-      if (m != cudaSuccess) return cuda_fail(h, m, "tick wrap");
-    }
-    h->p.tick = 2;
-  }
   return VBDR_OK;
+}
+
+vbdr_status vbdr_slide_delta(vbdr_t *h, const uint8_t *d_delta, uint64_t j0, uint64_t j1,
+                             void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (!h->fast) return fail(h, VBDR_ESTATE, "slide_delta exists only in layout fast");
+  if (!d_delta || (reinterpret_cast<uintptr_t>(d_delta) & 3u) || j0 >= j1 || j1 > h->p.n_phys ||
+      (j0 & 3u) || (j1 & 3u))
+    return fail(h, VBDR_EINVAL, "need a 4-byte aligned delta and 0 <= j0 < j1 <= n_phys, both multiples of 4");
+  if (vbdr_status s = check_async(h, "before slide_delta")) return s;
+  const cudaError_t e = vbdr_launch::slide_delta(h->p, d_delta, j0, j1, S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "slide_delta launch");
+  return after_slide(h, stream);
 }
 
 vbdr_status vbdr_estimate(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, double *d_out,

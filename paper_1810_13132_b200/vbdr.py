@@ -41,7 +41,7 @@ class vbdr_info_t(C.Structure):
 SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice", "vbdr_slide",
            "vbdr_estimate", "vbdr_host_sums", "vbdr_scan_slice_host", "vbdr_estimate_host",
            "vbdr_info", "vbdr_export_ages", "vbdr_export_ages_at", "vbdr_export_regmax",
-           "vbdr_export_pool_sums",
+           "vbdr_export_pool_sums", "vbdr_stamp_delta", "vbdr_slide_delta",
            "vbdr_last_error", "vbdr_status_string")
 
 _lib = None
@@ -68,6 +68,8 @@ def lib():
             "vbdr_estimate_host": [vp, vp, u64, vp, vp, vp, vp],
             "vbdr_info": [vp, C.POINTER(vbdr_info_t)],
             "vbdr_export_ages": [vp, vp, C.c_int, vp],
+            "vbdr_stamp_delta": [vp, vp, vp],
+            "vbdr_slide_delta": [vp, vp, u64, u64, vp],
             "vbdr_export_ages_at": [vp, vp, u64, vp, vp, C.c_int, vp],
             "vbdr_export_regmax": [vp, vp, vp],
             "vbdr_export_pool_sums": [vp, C.POINTER(u64), C.POINTER(u64), vp],
@@ -165,6 +167,18 @@ class VBDR:
         off = inf["off_sr"]
         return self.state[off:off + 4 * self.n_phys].view(torch.int32)
 
+    def regmax_view(self):
+        """The register values M[j] of the last boundary (uint8[n_phys] view)."""
+        off = self.info()["off_regmax"]
+        return self.state[off:off + self.n_phys]
+
+    def acc_view(self):
+        """(S_tot, V_tot) of the last closed slice as an int64[2] view."""
+        import torch
+        inf = self.info()
+        off = inf["off_acc"] + 16 * ((inf["tick"] - 1) & 1)
+        return self.state[off:off + 16].view(torch.int64)
+
     # --------------------------------------------------------------- the path
     def scan_slice(self, pairs, stream=None):
         """``vbdr_scan_slice``: pairs is a device uint32/int32 tensor of 2*n (aip, bip)."""
@@ -178,6 +192,22 @@ class VBDR:
         if group is not None:
             merge_stamps(self, group)
         self._check(lib().vbdr_slide(self._h, _stream_ptr(stream)), "vbdr_slide")
+
+    def stamp_delta(self, out=None, stream=None):
+        """``vbdr_stamp_delta``: this slice's max rank per BDR as uint8[n_phys]."""
+        import torch
+        if out is None:
+            out = torch.empty(self.n_phys, dtype=torch.uint8, device=self.device)
+        self._check(lib().vbdr_stamp_delta(self._h, C.c_void_p(out.data_ptr()),
+                                           _stream_ptr(stream)), "vbdr_stamp_delta")
+        return out
+
+    def slide_delta(self, delta, j0: int = 0, j1: int | None = None, stream=None):
+        """``vbdr_slide_delta``: close the slice from a merged delta over [j0, j1)."""
+        j1 = self.n_phys if j1 is None else j1
+        assert delta.is_cuda and delta.numel() >= j1 - j0
+        self._check(lib().vbdr_slide_delta(self._h, C.c_void_p(delta.data_ptr()), j0, j1,
+                                           _stream_ptr(stream)), "vbdr_slide_delta")
 
     def estimate(self, hosts, out=None, stream=None):
         """``vbdr_estimate``: hosts is a device uint32/int32 tensor; returns float64."""
@@ -287,3 +317,80 @@ def merge_stamps_tensor(sr, group=None):
 def merge_stamps(pool: "VBDR", group=None):
     """merge_stamps_tensor on the pool's stamp array (layout fast)."""
     return merge_stamps_tensor(pool.sr_view(), group)
+
+
+MERGE_MODES = ("stamps", "delta", "sharded")
+
+
+def _world(group):
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def reduce_scatter_max(full, shard, group=None):
+    """shard <- this rank's slice of the elementwise MAX of every rank's `full`
+    (NCCL reduce-scatter; all-reduce + copy on backends without it)."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.reduce_scatter_tensor(shard, full, op=dist.ReduceOp.MAX, group=group)
+    else:
+        world, rank = _world(group)
+        dist.all_reduce(full, op=dist.ReduceOp.MAX, group=group)
+        n = shard.numel()
+        shard.copy_(full[rank * n:(rank + 1) * n])
+    return shard
+
+
+def all_gather_shards(full, group=None):
+    """In place: every rank contributes its contiguous shard of `full`."""
+    import torch.distributed as dist
+    world, rank = _world(group)
+    n = full.numel() // world
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(full, full[rank * n:(rank + 1) * n], group=group)
+    else:
+        parts = list(full.split(n))
+        mine = parts[rank].clone()
+        dist.all_gather(parts, mine, group=group)
+    return full
+
+
+def slide_merged(pool: "VBDR", group=None, mode: str = "sharded", delta=None, shard=None):
+    """Close the slice on every rank after each scanned its own share of the
+    slice's pairs (pairs shard freely: the record is commutative and
+    idempotent, PAPER.md:297).
+
+    stamps : allreduce(MAX) of the u32 stamp arrays, full slide on every rank.
+    delta  : allreduce(MAX) of the u8 deltas (4x fewer bytes), full slide.
+    sharded: reduce-scatter(MAX) of the u8 deltas; each rank slides only its
+             1/N of the BDRs, then all-gathers the registers and all-reduces
+             the pool sums (bytes and slide time both /N).
+    With one rank this is vbdr_slide."""
+    import torch.distributed as dist
+    world, rank = _world(group)
+    if world <= 1:
+        pool.slide()
+        return
+    if mode == "stamps":
+        merge_stamps(pool, group)
+        pool.slide()
+        return
+    delta = pool.stamp_delta(delta)
+    if mode == "delta":
+        dist.all_reduce(delta, op=dist.ReduceOp.MAX, group=group)
+        pool.slide_delta(delta)
+        return
+    if mode != "sharded":
+        raise ValueError(f"merge mode {mode!r} not in {MERGE_MODES}")
+    n = pool.n_phys // world
+    if n * world != pool.n_phys or n % 4:
+        raise ValueError("sharded merge needs n_phys divisible by 4 * world size")
+    if shard is None:
+        import torch
+        shard = torch.empty(n, dtype=torch.uint8, device=delta.device)
+    reduce_scatter_max(delta, shard, group)
+    pool.slide_delta(shard, rank * n, (rank + 1) * n)
+    all_gather_shards(pool.regmax_view(), group)
+    dist.all_reduce(pool.acc_view(), op=dist.ReduceOp.SUM, group=group)

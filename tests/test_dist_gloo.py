@@ -14,7 +14,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_1810_13132_b200 import merge_stamps_tensor, shard_range
+from paper_1810_13132_b200 import (all_gather_shards, merge_stamps_tensor, reduce_scatter_max,
+                                   shard_range)
 
 
 def _free_port():
@@ -63,6 +64,26 @@ def _worker(rank, world, port, q):
         bufs = [torch.empty(e - s, dtype=torch.float64) for s, e in sizes]
         dist.all_gather(bufs, part)
         ok &= np.array_equal(torch.cat(bufs).numpy(), ref.estimate(M, hosts))
+        # sharded merge plumbing (slide_merged 'sharded'): reduce-scatter(MAX)
+        # of u8 nowLBP1 deltas, then an all-gather of per-rank register shards
+        tr2 = synth.CONFIGS["tiny"]
+        pairs = synth.generate(tr2, 9)
+        a, b = shard_range(len(pairs), rank, world)
+        mine = oracle.Pool(cfg, "serial")
+        mine.begin_slice()
+        mine.scan(pairs[a:b])
+        delta = torch.from_numpy(mine.now().copy())
+        n = cfg.z // world
+        shard = torch.empty(n, dtype=torch.uint8)
+        reduce_scatter_max(delta, shard)
+        whole = oracle.Pool(cfg, "serial")
+        whole.begin_slice()
+        whole.scan(pairs)
+        ok &= np.array_equal(shard.numpy(), whole.now()[rank * n:(rank + 1) * n])
+        regs = torch.zeros(cfg.z, dtype=torch.uint8)
+        regs[rank * n:(rank + 1) * n] = shard
+        all_gather_shards(regs)
+        ok &= np.array_equal(regs.numpy(), whole.now())
         # max-over-ranks timing reduction used by bench.py
         t_local = torch.tensor([1.0 + rank], dtype=torch.float64)
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)

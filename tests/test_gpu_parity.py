@@ -291,3 +291,69 @@ def test_loopback_multi_rank_merge(n_ranks):
         h0, h1 = shard_range(len(hosts_np), r, n_ranks)
         parts.append(pool.estimate(dev_u32(hosts_np[h0:h1])).cpu().numpy())
     check_estimates(np.concatenate(parts), ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
+
+
+@pytest.mark.parametrize("mode", ["delta", "sharded"])
+@pytest.mark.parametrize("n_ranks", [2, 8])
+def test_loopback_delta_merge(mode, n_ranks):
+    """The u8-delta merges of slide_merged, with the collectives emulated on one
+    GPU: 'delta' (elementwise max of the deltas, every rank slides all BDRs)
+    and 'sharded' (rank r slides only its 1/N of the BDRs from the merged
+    delta, then the registers are all-gathered and the pool sums all-reduced).
+    Every rank's registers, its shard's DR ages, the pool sums and the
+    host-sharded estimates are bit-exact / 1e-9 against the oracle."""
+    from paper_1810_13132_b200 import shard_range
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial")
+    ranks = [VBDR(32, 4, 1 << 12, device=DEV) for _ in range(n_ranks)]
+    n = cfg.z // n_ranks
+    hosts_np = tr.host_ids()
+    for t in range(7):
+        pairs = synth.generate(tr, t)
+        for r, pool in enumerate(ranks):
+            a, b = shard_range(len(pairs), r, n_ranks)
+            pool.scan_slice(dev_u32(pairs[a:b]))
+        deltas = [pool.stamp_delta() for pool in ranks]
+        merged = deltas[0].clone()
+        for d in deltas[1:]:
+            merged = torch.maximum(merged, d)
+        ref.slice(pairs)
+        if mode == "delta":
+            for pool in ranks:
+                pool.slide_delta(merged)
+        else:
+            for r, pool in enumerate(ranks):
+                pool.slide_delta(merged[r * n:(r + 1) * n].clone(), r * n, (r + 1) * n)
+            full = torch.cat([pool.regmax_view()[r * n:(r + 1) * n] for r, pool in enumerate(ranks)])
+            acc = sum(pool.acc_view() for pool in ranks)
+            for pool in ranks:
+                pool.regmax_view().copy_(full)
+                pool.acc_view().copy_(acc)
+        M = ref.readout()
+        drv = ref.drv()
+        for r, pool in enumerate(ranks):
+            assert np.array_equal(pool.export_regmax(), M)
+            assert pool.export_pool_sums() == oracle_pool_sums(M, cfg.L)
+            j0, j1 = (0, cfg.z) if mode == "delta" else (r * n, (r + 1) * n)
+            assert np.array_equal(pool.export_ages()[j0:j1], drv[j0:j1])
+    parts = []
+    for r, pool in enumerate(ranks):
+        h0, h1 = shard_range(len(hosts_np), r, n_ranks)
+        parts.append(pool.estimate(dev_u32(hosts_np[h0:h1])).cpu().numpy())
+    check_estimates(np.concatenate(parts), ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
+
+
+def test_delta_matches_stamps():
+    tr = synth.CONFIGS["tiny"]
+    pool = VBDR(32, 4, 1 << 12, device=DEV)
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    for t in range(3):
+        pairs = synth.generate(tr, t)
+        pool.scan_slice(dev_u32(pairs))
+        d = pool.stamp_delta().cpu().numpy()
+        o = oracle.Pool(cfg, "serial")
+        o.begin_slice()
+        o.scan(pairs)
+        assert np.array_equal(d, o.now())  # the paper's nowLBP1 (PAPER.md:184)
+        pool.slide()
