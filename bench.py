@@ -126,6 +126,17 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def wait_first(self, timeout: float = 5.0):
+        """Block until nvidia-smi wrote its first sample (it takes a while to start)."""
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < timeout:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    return
+            except OSError:
+                pass
+            time.sleep(0.02)
+
     def stop(self):
         if self.proc is None:
             return None
@@ -347,8 +358,10 @@ def run_vbdr(args):
         step(i)
     barrier()
 
-    # ---- device-resident timed region
+    # ---- device-resident timed region (clocks sampled through it and the e2e region)
     clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.wait_first()
     events = [[E() for _ in range(6)] for _ in range(args.steps)]
     launches0 = pool.info()["launches"]
     barrier()
@@ -357,7 +370,6 @@ def run_vbdr(args):
         step(args.warmup + i, events[i])
     barrier()
     launches = pool.info()["launches"] - launches0
-    clk = clocks.stop() if clocks else None
     ms = np.array([[ev[j].elapsed_time(ev[j + 1]) for j in range(5)] for ev in events])
     step_ms_local = ms.sum(axis=1)
     local_total = float(step_ms_local.sum())
@@ -412,6 +424,7 @@ def run_vbdr(args):
                "ms_per_step": e2e_ms / args.steps,
                "timing": "one CUDA-event region over all steps, copies pipelined across steps"}
 
+    clk = clocks.stop() if clocks else None
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

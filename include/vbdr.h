@@ -218,6 +218,11 @@ vbdr_status vbdr_export_regmax(vbdr_t *h, uint8_t *h_regmax, void *stream);
 vbdr_status vbdr_export_pool_sums(vbdr_t *h, uint64_t *h_S_tot, uint64_t *h_V_tot,
                                   void *stream);
 
+/* TEST ONLY.  Start a fresh pool (no slide yet) at slice tick `tick` (odd,
+ * < 2^26) so tests reach the stamp-tick wrap-around (every 2^26 slices) in a
+ * few slices.  Semantically a no-op: stamps are 0 and only compare to ticks. */
+vbdr_status vbdr_debug_set_tick(vbdr_t *h, uint32_t tick);
+
 const char *vbdr_last_error(const vbdr_t *h);
 const char *vbdr_status_string(vbdr_status s);
 

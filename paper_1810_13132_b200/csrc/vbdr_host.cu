@@ -339,6 +339,16 @@ vbdr_status vbdr_slide(vbdr_t *h, void *stream) {
   return after_slide(h, stream);
 }
 
+vbdr_status vbdr_debug_set_tick(vbdr_t *h, uint32_t tick) {
+  if (!h) return VBDR_EINVAL;
+  if (h->info.slices_closed != 0 || h->p.tick != 1)
+    return fail(h, VBDR_ESTATE, "the tick can only be set on a fresh pool");
+  if (tick < 1 || tick >= kTickLimit || (tick & 1u) != 1u)
+    return fail(h, VBDR_EINVAL, "tick must be odd and in [1, 2^26)");
+  h->p.tick = tick;  // fresh pool: every stamp is 0 < tick, accumulator parity kept
+  return VBDR_OK;
+}
+
 vbdr_status vbdr_stamp_delta(vbdr_t *h, uint8_t *d_delta, void *stream) {
   if (!h) return VBDR_EINVAL;
   if (!h->fast) return fail(h, VBDR_ESTATE, "stamp deltas exist only in layout fast");

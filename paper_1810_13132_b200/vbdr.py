@@ -41,7 +41,7 @@ class vbdr_info_t(C.Structure):
 SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice", "vbdr_slide",
            "vbdr_estimate", "vbdr_host_sums", "vbdr_scan_slice_host", "vbdr_estimate_host",
            "vbdr_info", "vbdr_export_ages", "vbdr_export_ages_at", "vbdr_export_regmax",
-           "vbdr_export_pool_sums", "vbdr_stamp_delta", "vbdr_slide_delta",
+           "vbdr_export_pool_sums", "vbdr_stamp_delta", "vbdr_slide_delta", "vbdr_debug_set_tick",
            "vbdr_last_error", "vbdr_status_string")
 
 _lib = None
@@ -69,6 +69,7 @@ def lib():
             "vbdr_info": [vp, C.POINTER(vbdr_info_t)],
             "vbdr_export_ages": [vp, vp, C.c_int, vp],
             "vbdr_stamp_delta": [vp, vp, vp],
+            "vbdr_debug_set_tick": [vp, u32],
             "vbdr_slide_delta": [vp, vp, u64, u64, vp],
             "vbdr_export_ages_at": [vp, vp, u64, vp, vp, C.c_int, vp],
             "vbdr_export_regmax": [vp, vp, vp],
@@ -166,6 +167,10 @@ class VBDR:
             raise RuntimeError("only the fast layout has mergeable stamps")
         off = inf["off_sr"]
         return self.state[off:off + 4 * self.n_phys].view(torch.int32)
+
+    def debug_set_tick(self, tick: int):
+        """``vbdr_debug_set_tick`` (tests only)."""
+        self._check(lib().vbdr_debug_set_tick(self._h, tick), "vbdr_debug_set_tick")
 
     def regmax_view(self):
         """The register values M[j] of the last boundary (uint8[n_phys] view)."""

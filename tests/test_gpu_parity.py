@@ -357,3 +357,47 @@ def test_delta_matches_stamps():
         o.scan(pairs)
         assert np.array_equal(d, o.now())  # the paper's nowLBP1
         pool.slide()
+
+
+@pytest.mark.parametrize("layout", ["fast", "packed"])
+def test_tick_wraparound(layout):
+    """Stamps are (T << 5) | rho with T < 2^26; at the limit the slide clears
+    the stamps and restarts T.  Parity must hold straight through the wrap."""
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(32, 4, 1 << 12, layout=layout, device=DEV)
+    pool.debug_set_tick((1 << 26) - 5)
+    hosts_np = tr.host_ids()
+    for t in range(10):
+        pairs = synth.generate(tr, t)
+        pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+        compare_boundary(pool, ref, [], hosts_np, dev_u32(hosts_np), None)
+    assert pool.info()["tick"] < 16
+
+
+def test_abi_errors():
+    """Argument and state errors are reported synchronously, nothing launched."""
+    pool = VBDR(32, 4, 1 << 12, device=DEV)
+    before = pool.info()["launches"]
+    bad = torch.zeros(9, dtype=torch.int32, device=DEV)[1:]  # 4-byte aligned only
+    with pytest.raises(RuntimeError, match="EINVAL"):
+        pool.scan_slice(bad)
+    with pytest.raises(RuntimeError, match="EINVAL"):
+        pool.slide_delta(torch.zeros(4096, dtype=torch.uint8, device=DEV), 0, 4097)
+    with pytest.raises(RuntimeError, match="EINVAL"):
+        pool.slide_delta(torch.zeros(4096, dtype=torch.uint8, device=DEV), 2, 10)
+    with pytest.raises(RuntimeError, match="ESTATE"):
+        VBDR(32, 4, 1 << 12, layout="packed", device=DEV).stamp_delta()
+    with pytest.raises(RuntimeError, match="EINVAL"):
+        pool.debug_set_tick(2)
+    pool.scan_slice(dev_u32(synth.generate(synth.CONFIGS["tiny"], 0)))
+    pool.slide()
+    with pytest.raises(RuntimeError, match="ESTATE"):
+        pool.debug_set_tick(101)
+    assert pool.info()["launches"] == before + 2
+    # empty inputs are legal no-ops
+    pool.scan_slice(torch.zeros(0, dtype=torch.int32, device=DEV))
+    assert pool.estimate(torch.zeros(0, dtype=torch.int32, device=DEV)).numel() == 0
