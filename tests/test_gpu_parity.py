@@ -386,7 +386,7 @@ def test_abi_errors():
     with pytest.raises(RuntimeError, match="EINVAL"):
         pool.scan_slice(bad)
     with pytest.raises(RuntimeError, match="EINVAL"):
-        pool.slide_delta(torch.zeros(4096, dtype=torch.uint8, device=DEV), 0, 4097)
+        pool.slide_delta(torch.zeros(8192, dtype=torch.uint8, device=DEV), 0, 4097)
     with pytest.raises(RuntimeError, match="EINVAL"):
         pool.slide_delta(torch.zeros(4096, dtype=torch.uint8, device=DEV), 2, 10)
     with pytest.raises(RuntimeError, match="ESTATE"):
