@@ -18,6 +18,10 @@ namespace {
 
 constexpr int kThreads = 256;
 
+#ifndef VBDR_SLIDE_SKIP
+#define VBDR_SLIDE_SKIP 1
+#endif
+
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
   return __ldcg(p);  // L2 (skip L1: other SMs update it)
 }
@@ -136,21 +140,36 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
       uint32_t xv[4] = {x[w].x, x[w].y, x[w].z, x[w].w};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t a;
+        uint32_t v = xv[c];
+        // A word whose fields are all saturated (== InitDR pattern) stays so
+        // under SlideDR and has no active field: skip its ALU work unless this
+        // slice's rank lands in it.  (Most high-rank words look like this.)
         if constexpr (FAST) {
-          uint32_t y = S::age(xv[c]);
+          uint32_t clr = 0u;
           if (hit[c] != 0u) {
             const uint32_t r = hit[c] - 1u;
             const uint32_t ws = r / (uint32_t)S::F;
-            if (ws == (uint32_t)w) y &= ~(S::FM << (ZB * (r - ws * (uint32_t)S::F)));
+            if (ws == (uint32_t)w) clr = S::FM << (ZB * (r - ws * (uint32_t)S::F));
           }
-          xv[c] = y;
-          a = S::active(y, addk);
+#if VBDR_SLIDE_SKIP
+          if (v == S::INIT && clr == 0u) continue;
+#endif
+          v = S::age(v) & ~clr;  // Alg.1: SlideDR every DR, then SetDR(DRV[nowLBP1])
+          xv[c] = v;
+          if (best[c] == 0u) {
+            const uint32_t a = S::active(v, addk);  // Alg.2 on the new ages
+            if (a != 0u) best[c] = (uint32_t)w * S::F + S::top_field(a) + 1u;
+          }
         } else {
-          a = S::active(xv[c], addk);
-          xv[c] = S::age(xv[c]);
+#if VBDR_SLIDE_SKIP
+          if (v == S::INIT) continue;
+#endif
+          if (best[c] == 0u) {
+            const uint32_t a = S::active(v, addk);  // Alg.2 on this boundary's ages
+            if (a != 0u) best[c] = (uint32_t)w * S::F + S::top_field(a) + 1u;
+          }
+          xv[c] = S::age(v);  // Alg.8 for the next slice
         }
-        if (best[c] == 0u && a != 0u) best[c] = (uint32_t)w * S::F + S::top_field(a) + 1u;
       }
       drv4[(uint64_t)w * n4 + q] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
     }

@@ -14,7 +14,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libvbdr.so")
+# VBDR_LIB points at an alternative build of the same library (kernel-variant
+# experiments in tools/); the default is the in-tree build.
+LIB_PATH = os.environ.get("VBDR_LIB") or os.path.join(_HERE, "_lib", "libvbdr.so")
 
 LAYOUT_FAST, LAYOUT_PACKED = 0, 1
 LAYOUTS = {"fast": LAYOUT_FAST, "packed": LAYOUT_PACKED}
