@@ -18,8 +18,12 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// Slide: 0 = SWAR on every word; 1 = skip warp-uniformly saturated words
+// entirely (fewer bytes than the algorithmic 8W per BDR); 2 = skip their ALU
+// work but still store them (default: the kernel moves exactly its
+// algorithmic bytes; profiles/r01_slide_variants.txt)
 #ifndef VBDR_SLIDE_SKIP
-#define VBDR_SLIDE_SKIP 1
+#define VBDR_SLIDE_SKIP 2
 #endif
 
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
@@ -138,38 +142,40 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
     for (int w = WM - 1; w >= 0; --w) {
       if (w >= (int)p.W) continue;
       uint32_t xv[4] = {x[w].x, x[w].y, x[w].z, x[w].w};
+      uint32_t clr[4] = {0u, 0u, 0u, 0u};  // FAST: the field Alg.1's SetDR clears in this word
+      bool sat = true;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t v = xv[c];
-        // A word whose fields are all saturated (== InitDR pattern) stays so
-        // under SlideDR and has no active field: skip its ALU work unless this
-        // slice's rank lands in it.  (Most high-rank words look like this.)
         if constexpr (FAST) {
-          uint32_t clr = 0u;
-          if (hit[c] != 0u) {
-            const uint32_t r = hit[c] - 1u;
-            const uint32_t ws = r / (uint32_t)S::F;
-            if (ws == (uint32_t)w) clr = S::FM << (ZB * (r - ws * (uint32_t)S::F));
-          }
-#if VBDR_SLIDE_SKIP
-          if (v == S::INIT && clr == 0u) continue;
-#endif
-          v = S::age(v) & ~clr;  // Alg.1: SlideDR every DR, then SetDR(DRV[nowLBP1])
-          xv[c] = v;
-          if (best[c] == 0u) {
-            const uint32_t a = S::active(v, addk);  // Alg.2 on the new ages
-            if (a != 0u) best[c] = (uint32_t)w * S::F + S::top_field(a) + 1u;
-          }
-        } else {
-#if VBDR_SLIDE_SKIP
-          if (v == S::INIT) continue;
-#endif
-          if (best[c] == 0u) {
-            const uint32_t a = S::active(v, addk);  // Alg.2 on this boundary's ages
-            if (a != 0u) best[c] = (uint32_t)w * S::F + S::top_field(a) + 1u;
-          }
-          xv[c] = S::age(v);  // Alg.8 for the next slice
+          const uint32_t r = hit[c] - 1u;
+          const uint32_t ws = r / (uint32_t)S::F;
+          clr[c] = (hit[c] != 0u && ws == (uint32_t)w) ? S::FM << (ZB * (r - ws * (uint32_t)S::F))
+                                                       : 0u;
         }
+        sat = sat && xv[c] == S::INIT && clr[c] == 0u;
+      }
+#if VBDR_SLIDE_SKIP
+      // Words whose fields are all saturated (the InitDR pattern) stay so
+      // under SlideDR and hold no active rank; when that is true for the whole
+      // warp (typical for the high-rank words) skip the SWAR work.
+      if (__all_sync(__activemask(), sat)) {
+#if VBDR_SLIDE_SKIP == 2
+        drv4[(uint64_t)w * n4 + q] = x[w];  // unchanged, stored anyway
+#endif
+        continue;  // VBDR_SLIDE_SKIP 1: unchanged words are not rewritten
+      }
+#endif
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t a;
+        if constexpr (FAST) {
+          xv[c] = S::age(xv[c]) & ~clr[c];  // Alg.1: SlideDR every DR, then SetDR(DRV[nowLBP1])
+          a = S::active(xv[c], addk);       // Alg.2 on the new ages
+        } else {
+          a = S::active(xv[c], addk);  // Alg.2 on this boundary's ages
+          xv[c] = S::age(xv[c]);       // Alg.8 for the next slice
+        }
+        if (best[c] == 0u && a != 0u) best[c] = (uint32_t)w * S::F + S::top_field(a) + 1u;
       }
       drv4[(uint64_t)w * n4 + q] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
     }
