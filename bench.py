@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--layout", default="fast", choices=["fast", "packed"])
     ap.add_argument("--scan-mode", type=int, default=0)
     ap.add_argument("--est-lanes", type=int, default=0)
-    ap.add_argument("--merge", default="sharded", choices=["stamps", "delta", "sharded"],
+    ap.add_argument("--merge", default="sharded", choices=["stamps", "delta", "sharded", "p2p"],
                     help="N>1 slide merge (paper_1810_13132_b200.slide_merged)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -261,8 +261,8 @@ def run_vbdr(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1810_13132_b200 import (VBDR, all_gather_shards, merge_stamps, reduce_scatter_max,
-                                       shard_range)
+    from paper_1810_13132_b200 import (VBDR, PeerMerge, all_gather_shards, make_config,
+                                       merge_stamps, reduce_scatter_max, shard_range)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -280,8 +280,12 @@ def run_vbdr(args):
     wl = WORKLOADS[args.config]
     if world > 1 and args.layout != "fast":
         raise SystemExit("multi-GPU needs --layout fast (NCCL has no bitwise-AND merge for packed)")
+    state = None
+    if world > 1 and args.merge == "p2p":  # pool state in symmetric memory (peer-writable)
+        state = PeerMerge.alloc_state(make_config(wl["m"], wl["k"], wl["n_phys"]), dev)
     pool = VBDR(wl["m"], wl["k"], wl["n_phys"], layout=args.layout, scan_mode=args.scan_mode,
-                est_lanes=args.est_lanes, device=dev)
+                est_lanes=args.est_lanes, device=dev, state=state)
+    peer = PeerMerge(pool, group) if state is not None else None
     info = pool.info()
     p0, p1 = shard_range(tr.pairs_per_slice, rank, world)
     h0, h1 = shard_range(tr.hosts, rank, world)
@@ -327,6 +331,13 @@ def run_vbdr(args):
             mark(evs, 2)
             pool.slide()
             mark(evs, 3)
+        elif args.merge == "p2p":
+            pool.stamp_delta(peer.delta)
+            peer._barrier()
+            mark(evs, 2)
+            pool.slide_peers(peer.peer_delta, peer.j0, peer.j1, peer.peer_regmax, peer.peer_acc)
+            mark(evs, 3)
+            peer._barrier()
         elif args.merge == "delta":
             pool.stamp_delta(delta_buf)
             dist.all_reduce(delta_buf, op=dist.ReduceOp.MAX, group=group)

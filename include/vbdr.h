@@ -160,6 +160,23 @@ vbdr_status vbdr_stamp_delta(vbdr_t *h, uint8_t *d_delta, void *stream);
 vbdr_status vbdr_slide_delta(vbdr_t *h, const uint8_t *d_delta, uint64_t j0, uint64_t j1,
                              void *stream);
 
+/* Fused merge + slide over peer memory (the B200 path: no collective kernel).
+ * h_peer_delta is a HOST array of n_peers (1..16) device pointers, one per
+ * rank, each to that rank's u8[n_phys] delta from vbdr_stamp_delta -- local or
+ * mapped over NVLink (CUDA IPC / symmetric memory).  The kernel merges the
+ * deltas of BDRs [j0, j1) with a per-byte max while sliding them.  If
+ * h_peer_regmax (n_peers pointers to every rank's regmax, vbdr_info
+ * off_regmax) is given, the register shard is written into every rank's
+ * regmax instead of only the local one; if h_peer_acc (n_peers pointers to
+ * every rank's accumulator base, vbdr_info off_acc) is given, the shard's pool
+ * sums are added atomically into every rank (own rank included in both
+ * lists).  The caller orders it between two cross-rank barriers: after every
+ * rank's vbdr_stamp_delta, and before any rank's vbdr_estimate.  Closes the
+ * slice like vbdr_slide. */
+vbdr_status vbdr_slide_peers(vbdr_t *h, const uint8_t *const *h_peer_delta, uint32_t n_peers,
+                             uint64_t j0, uint64_t j1, uint8_t *const *h_peer_regmax,
+                             uint64_t *const *h_peer_acc, void *stream);
+
 /* Estimate |OP(aip, t, k)| (Definition 1) for n_hosts hosts
  * over the window W(t-k+1..t) of the last closed slice: Alg.5 gather
  * (PAPER.md:197-213), HyperLogLog harmonic mean with linear counting, vHLL

@@ -105,13 +105,21 @@ k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict
 //   PACKED: M = GetLBP1BDR of the ages at this boundary (Alg.2), then age all
 //           DRs for the next slice (Alg.8 hoisted from the next slice open).
 // Writes regmax[j] = M and accumulates S_tot = sum 2^(L-M), V_tot = #{M=0}.
-// Multi-GPU: DELTA = true reads this slice's max ranks from a merged u8
-// array (delta4[q - q0] packs BDRs 4q..4q+3) instead of the local stamps, and
-// only BDR quads [q0, q1) are processed (the rank's shard).
-template <bool FAST, int ZB, bool DELTA>
+// Where this slice's max rank per BDR comes from (FAST layout only):
+//   SRC_STAMPS: the local stamps sr (one GPU, or after an allreduce of sr);
+//   SRC_DELTA:  a merged u8 array, delta4[q - q0] packing BDRs 4q..4q+3;
+//   SRC_PEERS:  the ranks' own u8 deltas read in place (NVLink peer memory on
+//               a multi-GPU box) and merged here with a per-byte max -- the
+//               merge is fused into the slide, no collective runs.  With
+//               peer register/accumulator pointers the kernel also writes its
+//               register shard and adds its pool sums into every rank.
+// Only BDR quads [q0, q1) are processed (the rank's shard).
+enum { SRC_STAMPS = 0, SRC_DELTA = 1, SRC_PEERS = 2 };
+
+template <bool FAST, int ZB, int SRC>
 __global__ void __launch_bounds__(kThreads)
 k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ delta4,
-        uint64_t q0, uint64_t q1) {
+        uint64_t q0, uint64_t q1, vbdr_launch::Peers peers) {
   using S = Swar<ZB>;
   constexpr int WM = WMax<ZB>::value;
   const uint64_t n4 = p.n_phys >> 2;
@@ -123,8 +131,14 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   for (uint64_t q = q0 + (uint64_t)blockIdx.x * kThreads + threadIdx.x; q < q1; q += stride) {
     uint32_t hit[4] = {0u, 0u, 0u, 0u};  // this slice's max rank of each BDR, or 0
-    if constexpr (FAST && DELTA) {
+    if constexpr (FAST && SRC == SRC_DELTA) {
       const uint32_t d = __ldcs(delta4 + (q - q0));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) hit[c] = (d >> (8 * c)) & 0xFFu;
+    } else if constexpr (FAST && SRC == SRC_PEERS) {
+      uint32_t d = 0u;
+      for (uint32_t r = 0; r < peers.n; ++r)
+        d = __vmaxu4(d, __ldcs(reinterpret_cast<const uint32_t *>(peers.delta[r]) + q));
 #pragma unroll
       for (int c = 0; c < 4; ++c) hit[c] = (d >> (8 * c)) & 0xFFu;
     } else if constexpr (FAST) {
@@ -179,7 +193,12 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
       }
       drv4[(uint64_t)w * n4 + q] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
     }
-    reg4[q] = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
+    const uint32_t r4 = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
+    if (SRC == SRC_PEERS && peers.n_regmax > 0) {
+      for (uint32_t r = 0; r < peers.n_regmax; ++r) reinterpret_cast<uint32_t *>(peers.regmax[r])[q] = r4;
+    } else {
+      reg4[q] = r4;
+    }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       s_acc += 1ull << (p.L - best[c]);
@@ -207,8 +226,15 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
       st += ss[w];
       vt += sv[w];
     }
-    atomicAdd(p.acc + 2 * slot, st);
-    atomicAdd(p.acc + 2 * slot + 1, vt);
+    if (SRC == SRC_PEERS && peers.n_acc > 0) {
+      for (uint32_t r = 0; r < peers.n_acc; ++r) {
+        atomicAdd(peers.acc[r] + 2 * slot, st);
+        atomicAdd(peers.acc[r] + 2 * slot + 1, vt);
+      }
+    } else {
+      atomicAdd(p.acc + 2 * slot, st);
+      atomicAdd(p.acc + 2 * slot + 1, vt);
+    }
     if (blockIdx.x == 0) {  // the other parity's slot is next slide's accumulator
       p.acc[2 * (slot ^ 1u)] = 0ull;
       p.acc[2 * (slot ^ 1u) + 1] = 0ull;
@@ -324,21 +350,25 @@ struct InitFn {
 template <int ZB>
 struct SlideFn {
   static cudaError_t run(const DevParams &p, bool fast, const uint32_t *delta4, uint64_t q0,
-                         uint64_t q1, cudaStream_t s) {
+                         uint64_t q1, const vbdr_launch::Peers *peers, cudaStream_t s) {
     // (2^zb - k) at every even field's LSB (Swar::active)
     uint32_t addk = 0;
     for (uint32_t f = 0; f < Swar<ZB>::F; f += 2) addk |= ((1u << ZB) - p.k) << (ZB * f);
     const uint32_t slot = p.tick & 1u;
     const uint64_t work = q1 - q0;
-    if (fast && delta4)
-      k_slide<true, ZB, true><<<grid_for(k_slide<true, ZB, true>, work), kThreads, 0, s>>>(
-          p, addk, slot, delta4, q0, q1);
+    const vbdr_launch::Peers none{};
+    if (fast && peers)
+      k_slide<true, ZB, SRC_PEERS><<<grid_for(k_slide<true, ZB, SRC_PEERS>, work), kThreads, 0, s>>>(
+          p, addk, slot, nullptr, q0, q1, *peers);
+    else if (fast && delta4)
+      k_slide<true, ZB, SRC_DELTA><<<grid_for(k_slide<true, ZB, SRC_DELTA>, work), kThreads, 0, s>>>(
+          p, addk, slot, delta4, q0, q1, none);
     else if (fast)
-      k_slide<true, ZB, false><<<grid_for(k_slide<true, ZB, false>, work), kThreads, 0, s>>>(
-          p, addk, slot, nullptr, q0, q1);
+      k_slide<true, ZB, SRC_STAMPS><<<grid_for(k_slide<true, ZB, SRC_STAMPS>, work), kThreads, 0, s>>>(
+          p, addk, slot, nullptr, q0, q1, none);
     else
-      k_slide<false, ZB, false><<<grid_for(k_slide<false, ZB, false>, work), kThreads, 0, s>>>(
-          p, addk, slot, nullptr, q0, q1);
+      k_slide<false, ZB, SRC_STAMPS><<<grid_for(k_slide<false, ZB, SRC_STAMPS>, work), kThreads, 0,
+                                       s>>>(p, addk, slot, nullptr, q0, q1, none);
     return cudaGetLastError();
   }
 };
@@ -378,13 +408,19 @@ cudaError_t init(const DevParams &p, bool fast, cudaStream_t s) {
 
 cudaError_t slide(const DevParams &p, bool fast, cudaStream_t s) {
   return dispatch_zb<SlideFn>(p.zb, p, fast, (const uint32_t *)nullptr, (uint64_t)0,
-                              p.n_phys >> 2, s);
+                              p.n_phys >> 2, (const Peers *)nullptr, s);
 }
 
 cudaError_t slide_delta(const DevParams &p, const uint8_t *delta, uint64_t j0, uint64_t j1,
                         cudaStream_t s) {
   return dispatch_zb<SlideFn>(p.zb, p, true, reinterpret_cast<const uint32_t *>(delta), j0 >> 2,
-                              j1 >> 2, s);
+                              j1 >> 2, (const Peers *)nullptr, s);
+}
+
+cudaError_t slide_peers(const DevParams &p, const Peers &peers, uint64_t j0, uint64_t j1,
+                        cudaStream_t s) {
+  return dispatch_zb<SlideFn>(p.zb, p, true, (const uint32_t *)nullptr, j0 >> 2, j1 >> 2, &peers,
+                              s);
 }
 
 cudaError_t delta(const DevParams &p, uint8_t *out, cudaStream_t s) {

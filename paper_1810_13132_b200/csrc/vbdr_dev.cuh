@@ -99,6 +99,15 @@ struct WMax {
 // Launchers implemented in the .cu files (host side, return cudaError_t).
 namespace vbdr_launch {
 using vbdr_dev::DevParams;
+
+// Peer pointers for the fused merge + slide (vbdr_slide_peers).
+constexpr int kMaxPeers = 16;
+struct Peers {
+  const uint8_t *delta[kMaxPeers];       // every rank's u8[n_phys] delta
+  uint8_t *regmax[kMaxPeers];            // every rank's regmax, or n_regmax = 0
+  unsigned long long *acc[kMaxPeers];    // every rank's accumulator base, or n_acc = 0
+  uint32_t n, n_regmax, n_acc;
+};
 cudaError_t init(const DevParams &p, bool fast, cudaStream_t s);
 cudaError_t scan(const DevParams &p, bool fast, int mode, const uint32_t *pairs, uint64_t n,
                  cudaStream_t s);
@@ -106,6 +115,8 @@ cudaError_t slide(const DevParams &p, bool fast, cudaStream_t s);
 cudaError_t slide_delta(const DevParams &p, const uint8_t *delta, uint64_t j0, uint64_t j1,
                         cudaStream_t s);
 cudaError_t delta(const DevParams &p, uint8_t *out, cudaStream_t s);
+cudaError_t slide_peers(const DevParams &p, const Peers &peers, uint64_t j0, uint64_t j1,
+                        cudaStream_t s);
 cudaError_t gather_words(const DevParams &p, const uint64_t *idx, uint64_t n, uint32_t *out,
                          cudaStream_t s);
 

@@ -374,6 +374,37 @@ vbdr_status vbdr_slide_delta(vbdr_t *h, const uint8_t *d_delta, uint64_t j0, uin
   return after_slide(h, stream);
 }
 
+vbdr_status vbdr_slide_peers(vbdr_t *h, const uint8_t *const *h_peer_delta, uint32_t n_peers,
+                             uint64_t j0, uint64_t j1, uint8_t *const *h_peer_regmax,
+                             uint64_t *const *h_peer_acc, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (!h->fast) return fail(h, VBDR_ESTATE, "slide_peers exists only in layout fast");
+  if (!h_peer_delta || n_peers < 1 || n_peers > (uint32_t)vbdr_launch::kMaxPeers || j0 >= j1 ||
+      j1 > h->p.n_phys || (j0 & 3u) || (j1 & 3u))
+    return fail(h, VBDR_EINVAL, "need 1..16 peer deltas and 0 <= j0 < j1 <= n_phys, multiples of 4");
+  vbdr_launch::Peers pe{};
+  pe.n = n_peers;
+  for (uint32_t r = 0; r < n_peers; ++r) {
+    if (!h_peer_delta[r] || (reinterpret_cast<uintptr_t>(h_peer_delta[r]) & 15u))
+      return fail(h, VBDR_EINVAL, "peer deltas must be 16-byte aligned device pointers");
+    pe.delta[r] = h_peer_delta[r];
+    if (h_peer_regmax) {
+      if (!h_peer_regmax[r]) return fail(h, VBDR_EINVAL, "null peer regmax");
+      pe.regmax[r] = h_peer_regmax[r];
+    }
+    if (h_peer_acc) {
+      if (!h_peer_acc[r]) return fail(h, VBDR_EINVAL, "null peer accumulator");
+      pe.acc[r] = reinterpret_cast<unsigned long long *>(h_peer_acc[r]);
+    }
+  }
+  pe.n_regmax = h_peer_regmax ? n_peers : 0;
+  pe.n_acc = h_peer_acc ? n_peers : 0;
+  if (vbdr_status s = check_async(h, "before slide_peers")) return s;
+  const cudaError_t e = vbdr_launch::slide_peers(h->p, pe, j0, j1, S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "slide_peers launch");
+  return after_slide(h, stream);
+}
+
 vbdr_status vbdr_estimate(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, double *d_out,
                           void *stream) {
   if (!h) return VBDR_EINVAL;

@@ -44,6 +44,7 @@ SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice",
            "vbdr_estimate", "vbdr_host_sums", "vbdr_scan_slice_host", "vbdr_estimate_host",
            "vbdr_info", "vbdr_export_ages", "vbdr_export_ages_at", "vbdr_export_regmax",
            "vbdr_export_pool_sums", "vbdr_stamp_delta", "vbdr_slide_delta", "vbdr_debug_set_tick",
+           "vbdr_slide_peers",
            "vbdr_last_error", "vbdr_status_string")
 
 _lib = None
@@ -72,6 +73,7 @@ def lib():
             "vbdr_export_ages": [vp, vp, C.c_int, vp],
             "vbdr_stamp_delta": [vp, vp, vp],
             "vbdr_debug_set_tick": [vp, u32],
+            "vbdr_slide_peers": [vp, vp, u32, u64, u64, vp, vp, vp],
             "vbdr_slide_delta": [vp, vp, u64, u64, vp],
             "vbdr_export_ages_at": [vp, vp, u64, vp, vp, C.c_int, vp],
             "vbdr_export_regmax": [vp, vp, vp],
@@ -119,7 +121,7 @@ class VBDR:
     def __init__(self, m: int, k: int, n_phys: int, *, seed_a0: int = 0x5EED0001,
                  seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
                  layout: str = "fast", scan_mode: int = 0, est_lanes: int = 0,
-                 est_pass_log2: int = 0, device=None, stream=None):
+                 est_pass_log2: int = 0, device=None, stream=None, state=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("VBDR needs a CUDA device (no CPU fallback)")
@@ -128,7 +130,11 @@ class VBDR:
                                est_lanes, est_pass_log2)
         nbytes = state_bytes(self.cfg)
         with torch.cuda.device(self.device):
-            self.state = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            if state is None:
+                state = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            # caller-provided state (e.g. symmetric memory for peer access)
+            assert state.dtype == torch.uint8 and state.numel() >= nbytes and state.is_cuda
+            self.state = state
             h = C.c_void_p()
             self._check(lib().vbdr_create(C.byref(self.cfg), C.c_void_p(self.state.data_ptr()),
                                           nbytes, _stream_ptr(stream), C.byref(h)), "vbdr_create")
@@ -215,6 +221,24 @@ class VBDR:
         assert delta.is_cuda and delta.numel() >= j1 - j0
         self._check(lib().vbdr_slide_delta(self._h, C.c_void_p(delta.data_ptr()), j0, j1,
                                            _stream_ptr(stream)), "vbdr_slide_delta")
+
+    def slide_peers(self, peer_delta, j0: int, j1: int, peer_regmax=None, peer_acc=None,
+                    stream=None):
+        """``vbdr_slide_peers``: fused merge + slide.  Each list holds one device
+        pointer (int) per rank, own rank included (see include/vbdr.h)."""
+        n = len(peer_delta)
+        arr = lambda xs: (C.c_void_p * n)(*[C.c_void_p(int(x)) for x in xs])  # noqa: E731
+        self._check(lib().vbdr_slide_peers(self._h, arr(peer_delta), n, j0, j1,
+                                           arr(peer_regmax) if peer_regmax is not None else None,
+                                           arr(peer_acc) if peer_acc is not None else None,
+                                           _stream_ptr(stream)), "vbdr_slide_peers")
+
+    def acc_ptr(self) -> int:
+        """Device address of the accumulator block (vbdr_info off_acc)."""
+        return self.state.data_ptr() + self.info()["off_acc"]
+
+    def regmax_ptr(self) -> int:
+        return self.state.data_ptr() + self.info()["off_regmax"]
 
     def estimate(self, hosts, out=None, stream=None):
         """``vbdr_estimate``: hosts is a device uint32/int32 tensor; returns float64."""
@@ -326,7 +350,7 @@ def merge_stamps(pool: "VBDR", group=None):
     return merge_stamps_tensor(pool.sr_view(), group)
 
 
-MERGE_MODES = ("stamps", "delta", "sharded")
+MERGE_MODES = ("stamps", "delta", "sharded", "p2p")
 
 
 def _world(group):
@@ -362,6 +386,55 @@ def all_gather_shards(full, group=None):
         mine = parts[rank].clone()
         dist.all_gather(parts, mine, group=group)
     return full
+
+
+class PeerMerge:
+    """Fused merge + slide over NVLink peer memory (``vbdr_slide_peers``).
+
+    Every rank's u8 delta and pool state live in torch symmetric memory, so
+    each rank's slide kernel reads its BDR shard of every peer's delta, merges
+    them with a per-byte max, slides the shard, and writes the register shard
+    and pool sums straight into every rank -- no reduce-scatter or all-gather
+    kernels.  Two stream-ordered barriers (tiny NCCL all-reduces) bracket it.
+    The pool must be created with ``state=PeerMerge.alloc_state(...)``.
+    Verified on one GPU with virtual peers (tests/test_gpu_parity.py); the
+    symmetric-memory rendezvous itself needs a multi-GPU box."""
+
+    @staticmethod
+    def alloc_state(cfg, device):
+        import torch.distributed._symmetric_memory as symm
+        import torch
+        return symm.empty(state_bytes(cfg), dtype=torch.uint8, device=device)
+
+    def __init__(self, pool: "VBDR", group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.pool, self.group = pool, group
+        self.world, self.rank = _world(group)
+        grp = group if group is not None else dist.group.WORLD
+        self.delta = symm.empty(pool.n_phys, dtype=torch.uint8, device=pool.device)
+        hd = symm.rendezvous(self.delta, grp)
+        hs = symm.rendezvous(pool.state, grp)
+        inf = pool.info()
+        self.peer_delta = [hd.buffer_ptrs[r] for r in range(self.world)]
+        self.peer_regmax = [hs.buffer_ptrs[r] + inf["off_regmax"] for r in range(self.world)]
+        self.peer_acc = [hs.buffer_ptrs[r] + inf["off_acc"] for r in range(self.world)]
+        self.flag = torch.zeros(1, dtype=torch.int32, device=pool.device)
+        n = pool.n_phys // self.world
+        if n * self.world != pool.n_phys or n % 4:
+            raise ValueError("p2p merge needs n_phys divisible by 4 * world size")
+        self.j0, self.j1 = self.rank * n, (self.rank + 1) * n
+
+    def _barrier(self):
+        import torch.distributed as dist
+        dist.all_reduce(self.flag, group=self.group)  # stream-ordered across ranks
+
+    def close_slice(self):
+        self.pool.stamp_delta(self.delta)
+        self._barrier()  # every rank's delta is written
+        self.pool.slide_peers(self.peer_delta, self.j0, self.j1, self.peer_regmax, self.peer_acc)
+        self._barrier()  # every rank's register shard and sums have landed
 
 
 def slide_merged(pool: "VBDR", group=None, mode: str = "sharded", delta=None, shard=None):

@@ -401,3 +401,50 @@ def test_abi_errors():
     # empty inputs are legal no-ops
     pool.scan_slice(torch.zeros(0, dtype=torch.int32, device=DEV))
     assert pool.estimate(torch.zeros(0, dtype=torch.int32, device=DEV)).numel() == 0
+
+
+@pytest.mark.parametrize("n_ranks", [2, 4, 8])
+def test_loopback_fused_peer_merge_slide(n_ranks):
+    """vbdr_slide_peers with virtual peers on one GPU: rank r's kernel reads
+    every rank's delta in place for its BDR shard, merges with a per-byte max,
+    slides the shard and writes registers and pool sums into every rank.  The
+    same kernel runs over NVLink-mapped peer pointers on a multi-GPU box."""
+    from paper_1810_13132_b200 import shard_range
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial")
+    ranks = [VBDR(32, 4, 1 << 12, device=DEV) for _ in range(n_ranks)]
+    deltas = [torch.empty(cfg.z, dtype=torch.uint8, device=DEV) for _ in range(n_ranks)]
+    n = cfg.z // n_ranks
+    regmax = [p.regmax_ptr() for p in ranks]
+    acc = [p.acc_ptr() for p in ranks]
+    hosts_np = tr.host_ids()
+    for t in range(7):
+        pairs = synth.generate(tr, t)
+        for r, pool in enumerate(ranks):
+            a, b = shard_range(len(pairs), r, n_ranks)
+            pool.scan_slice(dev_u32(pairs[a:b]))
+            pool.stamp_delta(deltas[r])
+        for r, pool in enumerate(ranks):
+            pool.slide_peers([d.data_ptr() for d in deltas], r * n, (r + 1) * n, regmax, acc)
+        ref.slice(pairs)
+        M = ref.readout()
+        drv = ref.drv()
+        for r, pool in enumerate(ranks):
+            assert np.array_equal(pool.export_regmax(), M)
+            assert pool.export_pool_sums() == oracle_pool_sums(M, cfg.L)
+            assert np.array_equal(pool.export_ages()[r * n:(r + 1) * n], drv[r * n:(r + 1) * n])
+    parts = []
+    for r, pool in enumerate(ranks):
+        h0, h1 = shard_range(len(hosts_np), r, n_ranks)
+        parts.append(pool.estimate(dev_u32(hosts_np[h0:h1])).cpu().numpy())
+    check_estimates(np.concatenate(parts), ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
+    # without peer register/accumulator lists it is a local merge + slide
+    solo = VBDR(32, 4, 1 << 12, device=DEV)
+    ref2 = oracle.Pool(cfg, "serial")
+    pairs = synth.generate(tr, 0)
+    solo.scan_slice(dev_u32(pairs))
+    d = solo.stamp_delta()
+    solo.slide_peers([d.data_ptr()], 0, cfg.z)
+    ref2.slice(pairs)
+    assert np.array_equal(solo.export_ages(), ref2.drv())
