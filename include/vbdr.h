@@ -80,8 +80,10 @@ typedef struct {
     uint32_t layout;
     /* scan_mode: 0 = default; 1 = plain atomic per pair; 2 = L2 load-check,
      * skip the atomic when the stored value already dominates; 3 = reserved
-     * (runs as 1); 4 = L1-cached load-check.  All modes give bit-identical
-     * state (stored values only move one way within a slice). */
+     * (runs as 1); 4 = L1-cached load-check; 5 = per-block shared-memory
+     * cache of recently updated words in front of the mode-2 check.  All
+     * modes give bit-identical state (stored values only move one way within
+     * a slice). */
     uint32_t scan_mode;
     /* est_lanes: lanes cooperating on one host in vbdr_estimate (1, 2, 4, 8,
      * 16 or 32; 0 = auto).  Tuning only; results are identical. */

@@ -31,16 +31,55 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
 }
 
 // ------------------------------------------------------------------ scan
+// MODE 5: a per-block direct-mapped cache in shared memory of (word, value
+// known to be in global memory).  Skewed traffic hits the same few thousand
+// registers again and again (Zipf super-spreaders); a cache hit that already
+// dominates skips both the global check and the atomic, saving the SM's
+// L1-to-L2 request slots that bound the scan.  An entry
+// is inserted only after its atomic was issued (or a load saw the value), so
+// it never exceeds what global memory will hold when the kernel ends.
+#ifndef VBDR_SCAN_CACHE_SLOTS
+#define VBDR_SCAN_CACHE_SLOTS 2048  // 16 KB per block
+#endif
+constexpr int kCacheSlots = VBDR_SCAN_CACHE_SLOTS;
+
+struct ScanCache {
+  unsigned long long e[kCacheSlots];  // (key << 32) | value; key = word index + 1 (0 = empty)
+};
+
+__device__ __forceinline__ bool cache_hit(const ScanCache *c, uint32_t key, uint32_t val, bool fast) {
+  const unsigned long long ent = c->e[key & (kCacheSlots - 1)];
+  if ((uint32_t)(ent >> 32) != key) return false;
+  const uint32_t v = (uint32_t)ent;
+  return fast ? v >= val : (v & val) == val;  // packed: val = field mask known cleared
+}
+
+__device__ __forceinline__ void cache_put(ScanCache *c, uint32_t key, uint32_t v) {
+  c->e[key & (kCacheSlots - 1)] = ((unsigned long long)key << 32) | v;
+}
+
 // One pair: Alg.4 lines 180-184 then the layout's record.
 template <bool FAST, int ZB, int MODE>
 __device__ __forceinline__ void record(uint32_t aip, uint32_t bip, const DevParams &p,
-                                       uint32_t tickbits) {
+                                       uint32_t tickbits, ScanCache *cache) {
   uint32_t pidx, rho;
   pair_index(aip, bip, p, pidx, rho);
   if constexpr (FAST) {
     // nowLBP1 <- max(nowLBP1, LBP1(bip'))
     const uint32_t val = tickbits | rho;
     uint32_t *a = p.sr + pidx;
+    if constexpr (MODE == 5) {
+      const uint32_t key = pidx + 1u;  // n_phys < 2^32 for this mode
+      if (cache_hit(cache, key, val, true)) return;
+      const uint32_t cur = ld_relaxed(a);
+      if (cur >= val) {
+        cache_put(cache, key, cur);
+        return;
+      }
+      atomicMax(a, val);
+      cache_put(cache, key, val);
+      return;
+    }
     if constexpr (MODE == 2) {
       if (ld_relaxed(a) >= val) return;  // stored value dominates: max is a no-op
     }
@@ -58,6 +97,19 @@ __device__ __forceinline__ void record(uint32_t aip, uint32_t bip, const DevPara
     const uint32_t f = r - w * (uint32_t)S::F;
     const uint32_t fm = S::FM << (ZB * f);
     uint32_t *a = p.drv + (uint64_t)w * p.n_phys + pidx;
+    if constexpr (MODE == 5) {
+      // value cached = mask of fields known to be zero in this word
+      const uint32_t key = (pidx << 4 | w) + 1u;  // n_phys <= 2^28, W <= 15 for this mode
+      if (cache_hit(cache, key, fm, false)) return;
+      const uint32_t cur = ld_relaxed(a);
+      uint32_t zero = 0u;  // fields of the word already zero
+#pragma unroll
+      for (int g = 0; g < S::F; ++g)
+        if (((cur >> (ZB * g)) & S::FM) == 0u) zero |= S::FM << (ZB * g);
+      if ((cur & fm) != 0u) atomicAnd(a, ~fm);
+      cache_put(cache, key, zero | fm);
+      return;
+    }
     if constexpr (MODE == 2) {
       if ((ld_relaxed(a) & fm) == 0u) return;  // already zero
     }
@@ -76,6 +128,13 @@ __global__ void __launch_bounds__(kThreads)
 k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict__ tail,
        DevParams p) {
   constexpr int UNROLL = 4;
+  ScanCache *cache = nullptr;
+  if constexpr (MODE == 5) {  // only this mode pays for the shared memory
+    __shared__ ScanCache cache_mem;
+    cache = &cache_mem;
+    for (int s = threadIdx.x; s < kCacheSlots; s += kThreads) cache->e[s] = 0ull;
+    __syncthreads();
+  }
   const uint32_t tickbits = p.tick << 5;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -85,17 +144,17 @@ k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict
     for (int u = 0; u < UNROLL; ++u) v[u] = __ldcs(pairs2 + i + u * stride);  // streamed once
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      record<FAST, ZB, MODE>(v[u].x, v[u].y, p, tickbits);
-      record<FAST, ZB, MODE>(v[u].z, v[u].w, p, tickbits);
+      record<FAST, ZB, MODE>(v[u].x, v[u].y, p, tickbits, cache);
+      record<FAST, ZB, MODE>(v[u].z, v[u].w, p, tickbits, cache);
     }
   }
   for (; i < n2; i += stride) {
     const uint4 v = __ldcs(pairs2 + i);
-    record<FAST, ZB, MODE>(v.x, v.y, p, tickbits);
-    record<FAST, ZB, MODE>(v.z, v.w, p, tickbits);
+    record<FAST, ZB, MODE>(v.x, v.y, p, tickbits, cache);
+    record<FAST, ZB, MODE>(v.z, v.w, p, tickbits, cache);
   }
   if (tail != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
-    record<FAST, ZB, MODE>(tail[0], tail[1], p, tickbits);
+    record<FAST, ZB, MODE>(tail[0], tail[1], p, tickbits, cache);
 }
 
 // ------------------------------------------------------------------ slide
@@ -383,6 +442,9 @@ cudaError_t launch_scan(const DevParams &p, int mode, const uint4 *pairs2, uint6
       break;
     case 4:
       k_scan<FAST, ZB, 4><<<grid_for(k_scan<FAST, ZB, 4>, work), kThreads, 0, s>>>(pairs2, n2, tail, p);
+      break;
+    case 5:
+      k_scan<FAST, ZB, 5><<<grid_for(k_scan<FAST, ZB, 5>, work), kThreads, 0, s>>>(pairs2, n2, tail, p);
       break;
     default:
       k_scan<FAST, ZB, 1><<<grid_for(k_scan<FAST, ZB, 1>, work), kThreads, 0, s>>>(pairs2, n2, tail, p);

@@ -63,7 +63,7 @@ std::string plan(const vbdr_config *c, vbdr_config *norm, Plan *pl) {
     n.seed_a1 = 0x5EED0002u;
   }
   if (n.layout > 1) return "layout must be 0 (fast) or 1 (packed)";
-  if (n.scan_mode > 4) return "scan_mode must be 0..4";
+  if (n.scan_mode > 5) return "scan_mode must be 0..5";
   if (n.est_lanes > 32 || (n.est_lanes & (n.est_lanes - 1)))
     return "est_lanes must be 0 or a power of two <= 32";
   if (n.est_pass_log2 > 32) return "est_pass_log2 must be 0..32";
@@ -129,11 +129,15 @@ vbdr_status check_async(vbdr *h, const char *where) {
 
 cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// scan_mode 0 picks the default (2: L2 load-check, fastest on the caida sweep,
-// profiles/r01_sweep_caida.jsonl); 3 (warp aggregation) is not built and runs as 1.
+// scan_mode 0 picks the default; 3 (warp aggregation) is not built and runs as 1.
 int scan_mode(const vbdr *h) {
-  const uint32_t m = h->cfg.scan_mode;
-  if (m == 0) return 2;
+  const uint32_t m0 = h->cfg.scan_mode;
+  // default: 5 for the stamps (fast), 2 for packed words (profiles/r01_scan_modes.txt)
+  const uint32_t m = m0 ? m0 : (h->fast ? 5u : 2u);
+  // mode 5 keys its shared-memory cache by word index: fast needs n_phys < 2^32,
+  // packed n_phys <= 2^28 (and W <= 15); otherwise use mode 2
+  if (m == 5 && (h->fast ? h->p.n_phys >= (1ull << 32) : (h->p.n_phys > (1ull << 28) || h->p.W > 15)))
+    return 2;
   return m == 3 ? 1 : (int)m;
 }
 

@@ -82,7 +82,7 @@ def compare_boundary(pool, ref: oracle.Pool, refs_other, hosts_np, hosts_dev, wi
 
 @pytest.mark.parametrize("layout", ["fast", "packed"])
 @pytest.mark.parametrize("scan_mode,est_lanes,passes", [(1, 0, 0), (2, 1, 0), (4, 8, 10), (1, 32, 0),
-                                                       (4, 2, 7), (0, 0, 11)])
+                                                       (4, 2, 7), (0, 0, 11), (5, 4, 0)])
 def test_tiny_every_boundary(layout, scan_mode, est_lanes, passes):
     """configs[0] 'tiny': 10k pairs/slice, 64 hosts, m=32, 2^12 BDRs, k=4."""
     tr = synth.CONFIGS["tiny"]
@@ -110,10 +110,11 @@ def test_tiny_every_boundary(layout, scan_mode, est_lanes, passes):
                          np.concatenate(slices[max(0, t - 3):t + 1]))
 
 
+@pytest.mark.parametrize("scan_mode", [0, 5])
 @pytest.mark.parametrize("layout", ["fast", "packed"])
 @pytest.mark.parametrize("k,m,n_phys", [(1, 2, 64), (3, 16, 1 << 10), (7, 64, 1 << 14),
                                         (15, 8, 1 << 8), (60, 256, 1 << 16), (300, 4, 1 << 9)])
-def test_configs_sweep_with_empty_slices(layout, k, m, n_phys):
+def test_configs_sweep_with_empty_slices(layout, k, m, n_phys, scan_mode):
     """Edge cases: k = 1 (discrete window), k = 2^zb - 1, big k (zb up to 9),
     g < 32 (several hosts per warp), empty slices, tiny pools."""
     b = m.bit_length() - 1
@@ -122,7 +123,7 @@ def test_configs_sweep_with_empty_slices(layout, k, m, n_phys):
     if layout == "packed" and (1 << cfg.zb) - 2 < k:
         cfg = oracle.PoolConfig(b=b, k=k, z=n_phys, zb=cfg.zb + 1)
     ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
-    pool = VBDR(m, k, n_phys, layout=layout, device=DEV)
+    pool = VBDR(m, k, n_phys, layout=layout, scan_mode=scan_mode, device=DEV)
     assert pool.info()["zbits"] == cfg.zb
     hosts_np = tr.host_ids()
     hosts = dev_u32(hosts_np)
@@ -176,7 +177,7 @@ def test_negative_control_skipped_slide_breaks_parity():
 def test_order_split_and_duplicates_give_identical_state():
     tr = synth.CONFIGS["tiny"]
     a = VBDR(32, 4, 1 << 12, device=DEV)
-    b = VBDR(32, 4, 1 << 12, device=DEV, scan_mode=2)
+    b = VBDR(32, 4, 1 << 12, device=DEV, scan_mode=5)
     rng = np.random.default_rng(0)
     for t in range(5):
         pairs = synth.generate(tr, t)
@@ -223,8 +224,9 @@ def test_synth_cuda_twin_matches_numpy():
             assert np.array_equal(got, synth.generate(tr, t, start, count))
 
 
-@pytest.mark.parametrize("layout,pass_log2", [("fast", 0), ("packed", 0), ("fast", 20)])
-def test_caida_full_size(layout, pass_log2):
+@pytest.mark.parametrize("layout,pass_log2,scan_mode", [("fast", 0, 0), ("packed", 0, 0),
+                                                       ("fast", 20, 5), ("packed", 0, 5)])
+def test_caida_full_size(layout, pass_log2, scan_mode):
     """configs[1] 'caida' at full size (5M pairs/slice, 2^22 BDRs, m=128, k=5,
     500k hosts) in the launch configuration bench.py times: every register,
     the pool sums and all 500k host sums bit-exact, all estimates to 1e-9,
@@ -232,7 +234,8 @@ def test_caida_full_size(layout, pass_log2):
     tr = synth.CONFIGS["caida"]
     cfg = oracle.PoolConfig(b=7, k=5, z=1 << 22)
     ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
-    pool = VBDR(128, 5, 1 << 22, layout=layout, est_pass_log2=pass_log2, device=DEV)
+    pool = VBDR(128, 5, 1 << 22, layout=layout, est_pass_log2=pass_log2, scan_mode=scan_mode,
+                device=DEV)
     hosts_np = tr.host_ids()
     hosts = dev_u32(hosts_np)
     rng = np.random.default_rng(5)
