@@ -403,7 +403,8 @@ def run_vbdr(args):
         h_inputs = [inputs[i].cpu().pin_memory() for i in range(min(n_inputs, 4))]
         h_hosts = torch.from_numpy(hosts_all[h0:h1].view(np.int32)).pin_memory()
         h_out = torch.empty(h1 - h0, dtype=torch.float64).pin_memory()
-        stage = torch.empty(2 * min(n_local, 1 << 21), dtype=torch.int32, device=dev)
+        # two halves of a whole slice each: the next slice's copy overlaps this slice's compute
+        stage = torch.empty(2 * 2 * n_local, dtype=torch.int32, device=dev)
         hstage = torch.empty(max(h1 - h0, 1), dtype=torch.int32, device=dev)
         ostage = torch.empty(max(h1 - h0, 1), dtype=torch.float64, device=dev)
 
