@@ -206,9 +206,10 @@ vbdr_status vbdr_host_sums(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
 vbdr_status vbdr_scan_slice_host(vbdr_t *h, const uint32_t *h_pairs, uint64_t n_pairs,
                                  uint32_t *d_stage, uint64_t stage_pairs, void *stream);
 
-/* vbdr_estimate on HOST buffers: copies h_hosts into d_hosts_stage, runs the
- * estimate into d_out_stage and copies the results into h_out.
- * Stream-ordered; h_out is valid after the stream is synchronised. */
+/* vbdr_estimate on HOST buffers: copies h_hosts into d_hosts_stage on the
+ * internal copy stream (behind earlier pair copies, never behind compute), runs
+ * the estimate into d_out_stage on `stream` and copies the results into h_out.
+ * Stream-ordered; h_out is valid after `stream` is synchronised. */
 vbdr_status vbdr_estimate_host(vbdr_t *h, const uint32_t *h_hosts, uint64_t n_hosts,
                                uint32_t *d_hosts_stage, double *d_out_stage,
                                double *h_out, void *stream);

@@ -24,6 +24,8 @@ struct vbdr {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_scanned[2] = {nullptr, nullptr};
+  cudaEvent_t ev_hosts_in = nullptr;    // host ids copied (copy stream)
+  cudaEvent_t ev_hosts_free = nullptr;  // last estimate that read the host stage
 };
 
 namespace {
@@ -194,6 +196,9 @@ vbdr_status ensure_pipeline(vbdr *h, cudaStream_t cs) {
     // "slot i is free" starts out as: everything queued on the caller's stream so far
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_scanned[i], cs);
   }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_hosts_in, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_hosts_free, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(h->ev_hosts_free, cs);
   if (e != cudaSuccess) return cuda_fail(h, e, "pipeline resources");
   return VBDR_OK;
 }
@@ -311,6 +316,8 @@ vbdr_status vbdr_destroy(vbdr_t *h) {
     if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
     if (h->ev_scanned[i]) cudaEventDestroy(h->ev_scanned[i]);
   }
+  if (h->ev_hosts_in) cudaEventDestroy(h->ev_hosts_in);
+  if (h->ev_hosts_free) cudaEventDestroy(h->ev_hosts_free);
   delete h;
   return VBDR_OK;
 }
@@ -484,18 +491,28 @@ vbdr_status vbdr_estimate_host(vbdr_t *h, const uint32_t *h_hosts, uint64_t n_ho
   if (n_hosts == 0) return VBDR_OK;
   if (!h_hosts || !d_hosts_stage || !d_out_stage || !h_out)
     return fail(h, VBDR_EINVAL, "null pointer");
-  if (vbdr_status s = check_async(h, "before estimate_host")) return s;
   cudaStream_t cs = S(stream);
-  cudaError_t e =
-      cudaMemcpyAsync(d_hosts_stage, h_hosts, 4ull * n_hosts, cudaMemcpyHostToDevice, cs);
+  if (vbdr_status s = ensure_pipeline(h, cs)) return s;
+  if (vbdr_status s = check_async(h, "before estimate_host")) return s;
+  // The host ids travel on the copy stream like the pairs (all host-to-device
+  // traffic in one FIFO, never queued behind compute); the estimate waits for
+  // them, the next copy into the stage waits for the estimate that read it.
+  cudaError_t e = cudaStreamWaitEvent(h->copy_stream, h->ev_hosts_free, 0);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_hosts_stage, h_hosts, 4ull * n_hosts, cudaMemcpyHostToDevice,
+                        h->copy_stream);
+  if (e == cudaSuccess) e = cudaEventRecord(h->ev_hosts_in, h->copy_stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, h->ev_hosts_in, 0);
   uint32_t nl = 0;
   if (e == cudaSuccess)
     e = vbdr_launch::estimate(est_params(h), d_hosts_stage, n_hosts, d_out_stage, nullptr,
                               nullptr, cs, &nl);
   if (e == cudaSuccess) {
     h->info.launches += nl;
-    e = cudaMemcpyAsync(h_out, d_out_stage, 8ull * n_hosts, cudaMemcpyDeviceToHost, cs);
+    e = cudaEventRecord(h->ev_hosts_free, cs);
   }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h_out, d_out_stage, 8ull * n_hosts, cudaMemcpyDeviceToHost, cs);
   if (e != cudaSuccess) return cuda_fail(h, e, "estimate_host");
   return VBDR_OK;
 }
