@@ -101,6 +101,13 @@ def _declare(L):
                                u32p, C.c_uint64, u8p]),
         "orc_memory_bits": (C.c_uint64, [C.c_int, C.c_uint32, C.c_uint32]),
         "orc_estimate_M": (None, [C.c_uint32, C.c_uint32, C.c_uint64, u8p, u32p, C.c_uint64, f64p]),
+        "orc_bdr_pcsa_R": (C.c_uint32, [u16p, C.c_uint32, C.c_uint32]),
+        "orc_readout_pcsa": (None, [C.c_void_p, u8p]),
+        "orc_loglog_alpha": (C.c_double, [C.c_uint64]),
+        "orc_loglog_raw": (C.c_double, [u8p, C.c_uint64]),
+        "orc_pcsa_raw": (C.c_double, [u8p, C.c_uint64]),
+        "orc_estimate_variant": (None, [C.c_uint32, C.c_uint32, C.c_uint64, u8p, u32p, C.c_uint64,
+                                        C.c_int, f64p]),
         "orc_host_sums_M": (None, [C.c_uint32, C.c_uint32, C.c_uint64, u8p, u32p, C.c_uint64,
                                    f64p, u64p]),
     }
@@ -181,6 +188,40 @@ def estimate_M(M: np.ndarray, hosts: np.ndarray, b: int, z: int, A0: int = 0x5EE
     hosts = np.ascontiguousarray(hosts, dtype=np.uint32)
     out = np.empty(hosts.size, dtype=np.float64)
     lib().orc_estimate_M(b, A0, z, _ptr(M, u8p), _ptr(hosts, u32p), hosts.size, _ptr(out, f64p))
+    return out
+
+
+ESTIMATORS = {"hll": 0, "loglog": 1, "pcsa": 2}
+
+
+def loglog_alpha(m: int) -> float:
+    return lib().orc_loglog_alpha(m)
+
+
+def loglog_raw(M: np.ndarray) -> float:
+    M = np.ascontiguousarray(M, dtype=np.uint8)
+    return lib().orc_loglog_raw(_ptr(M, u8p), M.size)
+
+
+def pcsa_raw(R: np.ndarray) -> float:
+    R = np.ascontiguousarray(R, dtype=np.uint8)
+    return lib().orc_pcsa_raw(_ptr(R, u8p), R.size)
+
+
+def bdr_pcsa_R(drv: np.ndarray, k: int) -> int:
+    d = np.ascontiguousarray(drv, dtype=np.uint16)
+    return lib().orc_bdr_pcsa_R(_ptr(d, u16p), d.size, k)
+
+
+def estimate_variant(V: np.ndarray, hosts: np.ndarray, b: int, z: int, estimator: str,
+                     A0: int = 0x5EED0001) -> np.ndarray:
+    """Per-host estimates with register values V under 'hll', 'loglog' (V = M)
+    or 'pcsa' (V = R), noise-subtracted as vHLL (R#15)."""
+    V = np.ascontiguousarray(V, dtype=np.uint8)
+    hosts = np.ascontiguousarray(hosts, dtype=np.uint32)
+    out = np.empty(hosts.size, dtype=np.float64)
+    lib().orc_estimate_variant(b, A0, z, _ptr(V, u8p), _ptr(hosts, u32p), hosts.size,
+                               ESTIMATORS[estimator], _ptr(out, f64p))
     return out
 
 
@@ -305,6 +346,13 @@ class Pool:
         out = np.empty(self.cfg.z, dtype=np.uint8)
         lib().orc_export_now(self._h, _ptr(out, u8p))
         return out
+
+    def readout_pcsa(self) -> np.ndarray:
+        """PCSA registers R[j] (meaningful for the gsmall variant, which records
+        every rank: the sliding bitmap)."""
+        R = np.empty(self.cfg.z, dtype=np.uint8)
+        lib().orc_readout_pcsa(self._h, _ptr(R, u8p))
+        return R
 
     def ck(self) -> np.ndarray:
         """Canonical state C_k[j][r] = min(DR, k)."""

@@ -411,6 +411,80 @@ void orc_host_sums(const orc_pool *p, const uint8_t *M, const uint32_t *hosts,
 }
 
 /* ------------------------------------------------------------------ */
+/* Method variants: the BDR pool under other        */
+/* register estimators                                                  */
+/* ------------------------------------------------------------------ */
+
+/* PCSA register of one BDR under a sliding window.  PCSA (Flajolet-Martin,
+ * PAPER.md:58) keeps a bitmap per register and reads R = the position of its
+ * lowest zero bit.  "BDRP could also be used in PCSA ... by replacing its
+ * nowLBP1 with the value recorded in other algorithms": the
+ * sliding bitmap is {r : DRV[r] active} -- which needs every rank recorded,
+ * i.e. the gsmall DRV (Alg.9).  R = (lowest inactive rank) - 1, or L when all
+ * L ranks are active. */
+uint32_t orc_bdr_pcsa_R(const uint16_t *drv, uint32_t L, uint32_t k)
+{
+    for (uint32_t r = 1; r <= L; ++r)
+        if (!orc_IsActiveDR(drv[r - 1], k)) return r - 1;
+    return L;
+}
+
+void orc_readout_pcsa(const orc_pool *p, uint8_t *R)
+{
+    for (uint64_t j = 0; j < p->z; ++j)
+        R[j] = (uint8_t)orc_bdr_pcsa_R(&p->drv[j * p->L], p->L, p->k);
+}
+
+/* LogLog bias constant (Durand & Flajolet 2003):
+ *   alpha_m = (Gamma(-1/m) (1 - 2^(1/m)) / ln 2)^(-m).
+ * Both factors are negative; written in logs,
+ *   alpha_m = exp(-m [ln|Gamma(-1/m)| + ln(2^(1/m) - 1) - ln ln 2]),
+ * with 2^(1/m) - 1 = expm1(ln2 / m) so large m does not cancel digits. */
+double orc_loglog_alpha(uint64_t m)
+{
+    double x = 1.0 / (double)m;
+    double lb = lgamma(-x) + log(expm1(x * log(2.0))) - log(log(2.0));
+    return exp(-(double)m * lb);
+}
+
+/* LogLog raw estimate from the register values: alpha_s s 2^(sum M / s) --
+ * the geometric-mean estimator that consumes exactly Alg.5's sum of LBP1
+ * (PAPER.md:195-213, 60). */
+double orc_loglog_raw(const uint8_t *M, uint64_t s)
+{
+    uint64_t sum = 0;
+    for (uint64_t j = 0; j < s; ++j) sum += M[j];
+    return orc_loglog_alpha(s) * (double)s * pow(2.0, (double)sum / (double)s);
+}
+
+/* PCSA raw estimate: (s / phi) 2^(sum R / s), phi = 0.77351 (Flajolet-Martin). */
+double orc_pcsa_raw(const uint8_t *R, uint64_t s)
+{
+    uint64_t sum = 0;
+    for (uint64_t j = 0; j < s; ++j) sum += R[j];
+    return ((double)s / 0.77351) * pow(2.0, (double)sum / (double)s);
+}
+
+/* Per-host estimates with a chosen register estimator (0 HLL, 1 LogLog,
+ * 2 PCSA) on register values V (M for HLL/LogLog, R for PCSA), combined with
+ * the same shared-pool noise subtraction as orc_vhll (R#15). */
+void orc_estimate_variant(uint32_t b, uint32_t A0, uint64_t z, const uint8_t *V,
+                          const uint32_t *hosts, uint64_t n, int estimator, double *out)
+{
+    uint32_t g = 1u << b;
+    double E_tot = estimator == 0 ? orc_hll_raw(V, z)
+                 : estimator == 1 ? orc_loglog_raw(V, z) : orc_pcsa_raw(V, z);
+    uint8_t *regs = (uint8_t *)malloc(g);
+    for (uint64_t h = 0; h < n; ++h) {
+        for (uint32_t i = 0; i < g; ++i) regs[i] = V[orc_getPhyIdx(hosts[h], i, A0, z)];
+        double E_s = estimator == 0 ? orc_hll_raw(regs, g)
+                   : estimator == 1 ? orc_loglog_raw(regs, g) : orc_pcsa_raw(regs, g);
+        out[h] = orc_vhll(z, g, E_s, E_tot);
+    }
+    free(regs);
+}
+
+/* ------------------------------------------------------------------ */
 /* Independent references                                               */
 /* ------------------------------------------------------------------ */
 

@@ -146,3 +146,127 @@ def test_fresh_pool_estimates_zero():
     p = oracle.Pool(cfg, "serial")
     est = p.estimate(p.readout(), np.arange(100, dtype=np.uint32))
     assert (est == 0).all()
+
+
+# ---------------------------------------------------------------- N4 variants
+def test_loglog_alpha_limit_and_monotone():
+    """Durand-Flajolet alpha_m -> e^-gamma / sqrt(2) = 0.39701... (closed form),
+    from below, with a 1/m approach."""
+    import math
+    a_inf = math.exp(-0.5772156649015329) / math.sqrt(2)
+    prev = 0.0
+    for e in range(4, 23):
+        m = 1 << e
+        a = oracle.loglog_alpha(m)
+        assert prev < a < a_inf
+        assert abs(a / a_inf - 1) < 2.0 / m
+        prev = a
+
+
+def test_loglog_pcsa_closed_forms():
+    # all registers equal to r: LogLog = alpha_s s 2^r; PCSA = (s / 0.77351) 2^r
+    for s, r in ((32, 0), (32, 3), (128, 5)):
+        regs = np.full(s, r, np.uint8)
+        assert oracle.loglog_raw(regs) == pytest.approx(oracle.loglog_alpha(s) * s * 2.0 ** r,
+                                                        rel=1e-15)
+        assert oracle.pcsa_raw(regs) == pytest.approx(s / 0.77351 * 2.0 ** r, rel=1e-15)
+    # mixed: geometric mean of 2^M over the registers
+    regs = np.array([0, 2] * 16, np.uint8)
+    assert oracle.loglog_raw(regs) == pytest.approx(oracle.loglog_alpha(32) * 32 * 2.0, rel=1e-15)
+
+
+def test_pcsa_readout_traces():
+    k, zb, L = 4, 3, 10
+    S = (1 << zb) - 1
+    d = np.full(L, S)
+    assert oracle.bdr_pcsa_R(d, k) == 0            # nothing active
+    d[0] = d[1] = 0
+    d[3] = 1                                       # ranks 1, 2, 4 active; 3 not
+    assert oracle.bdr_pcsa_R(d, k) == 2
+    d[2] = k                                       # rank 3 expired: still 2
+    assert oracle.bdr_pcsa_R(d, k) == 2
+    d[2] = k - 1
+    assert oracle.bdr_pcsa_R(d, k) == 4            # 1..4 active, 5 not
+    assert oracle.bdr_pcsa_R(np.zeros(L), k) == L  # all active
+
+
+def _textbook_bitmaps(bips, b, L, A1):
+    """Flajolet-Martin PCSA for ONE host: register vidx collects the set of
+    ranks seen; R = lowest missing rank - 1 (int.bit_length for the rank)."""
+    seen = [set() for _ in range(1 << b)]
+    for bip in bips:
+        h = oracle.H(int(bip), 1 << 32, A1)
+        w = (h << b) & 0xFFFFFFFF
+        seen[h >> (32 - b)].add(min(33 - w.bit_length() if w else 33, L))
+    R = []
+    for st in seen:
+        r = 1
+        while r in st and r <= L:
+            r += 1
+        R.append(r - 1)
+    return np.array(R, np.uint8)
+
+
+def test_pcsa_gsmall_pool_is_textbook_pcsa_and_sliding():
+    """One host alone in a gsmall pool: the gathered PCSA registers equal a
+    textbook FM bitmap readout; the RMS error of the PCSA raw estimate is
+    ~0.78/sqrt(g); after slides the registers equal the bitmaps of the window's
+    pairs only (sliding correctness of the PCSA readout)."""
+    b, g = 5, 32
+    cfg = oracle.PoolConfig(b=b, k=3, z=1 << 15)
+    rng = np.random.default_rng(31)
+    errs = []
+    for s in range(40):
+        aip = int(rng.integers(0, 1 << 32))
+        if len({oracle.getPhyIdx(aip, i, cfg.A0, cfg.z) for i in range(g)}) < g:
+            continue
+        n = 4000
+        bips = rng.choice(1 << 32, size=n, replace=False).astype(np.uint32)
+        p = oracle.Pool(cfg, "gsmall")
+        p.slice(np.stack([np.full(n, aip, np.uint32), bips], axis=1))
+        regs = p.gather(p.readout_pcsa(), aip)
+        if s < 6:
+            assert np.array_equal(regs, _textbook_bitmaps(bips, b, cfg.L, cfg.A1))
+        errs.append(oracle.pcsa_raw(regs) / n - 1)
+        if s < 3:  # slide k more slices with other peers: only the window counts
+            later = []
+            for t in range(cfg.k):
+                nb = rng.choice(1 << 32, size=500, replace=False).astype(np.uint32)
+                later.append(nb)
+                p.slice(np.stack([np.full(nb.size, aip, np.uint32), nb], axis=1))
+            regs = p.gather(p.readout_pcsa(), aip)
+            assert np.array_equal(regs, _textbook_bitmaps(np.concatenate(later), b, cfg.L,
+                                                          cfg.A1))
+    rms = float(np.sqrt(np.mean(np.square(errs))))
+    assert 0.6 * 0.78 / np.sqrt(g) <= rms <= 1.5 * 0.78 / np.sqrt(g), rms
+
+
+def test_loglog_textbook_special_case():
+    """One host alone: LogLog on the gathered registers has RMS ~1.30/sqrt(g)."""
+    b, g = 6, 64
+    cfg = oracle.PoolConfig(b=b, k=3, z=1 << 16)
+    rng = np.random.default_rng(17)
+    errs = []
+    for _ in range(40):
+        aip = int(rng.integers(0, 1 << 32))
+        n = 20000
+        bips = rng.choice(1 << 32, size=n, replace=False).astype(np.uint32)
+        p = oracle.Pool(cfg, "serial")
+        p.slice(np.stack([np.full(n, aip, np.uint32), bips], axis=1))
+        errs.append(oracle.loglog_raw(p.gather(p.readout(), aip)) / n - 1)
+    rms = float(np.sqrt(np.mean(np.square(errs))))
+    assert 0.6 * 1.30 / np.sqrt(g) <= rms <= 1.5 * 1.30 / np.sqrt(g), rms
+
+
+def test_estimate_variant_hll_matches_pool_estimate():
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    tr = synth.CONFIGS["tiny"]
+    p = oracle.Pool(cfg, "gsmall")
+    for t in range(5):
+        p.slice(synth.generate(tr, t))
+    M = p.readout()
+    hosts = tr.host_ids()
+    assert np.array_equal(oracle.estimate_variant(M, hosts, cfg.b, cfg.z, "hll"),
+                          p.estimate(M, hosts))
+    est = oracle.estimate_variant(p.readout_pcsa(), hosts, cfg.b, cfg.z, "pcsa")
+    assert (est >= 0).all() and est.max() > 100
