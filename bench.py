@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--layout", default="fast", choices=["fast", "packed"])
     ap.add_argument("--scan-mode", type=int, default=0)
     ap.add_argument("--est-lanes", type=int, default=0)
+    ap.add_argument("--estimator", default="hll", choices=["hll", "loglog", "pcsa"])
     ap.add_argument("--merge", default="sharded", choices=["stamps", "delta", "sharded", "p2p"],
                     help="N>1 slide merge (paper_1810_13132_b200.slide_merged)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -284,7 +285,7 @@ def run_vbdr(args):
     if world > 1 and args.merge == "p2p":  # pool state in symmetric memory (peer-writable)
         state = PeerMerge.alloc_state(make_config(wl["m"], wl["k"], wl["n_phys"]), dev)
     pool = VBDR(wl["m"], wl["k"], wl["n_phys"], layout=args.layout, scan_mode=args.scan_mode,
-                est_lanes=args.est_lanes, device=dev, state=state)
+                est_lanes=args.est_lanes, estimator=args.estimator, device=dev, state=state)
     peer = PeerMerge(pool, group) if state is not None else None
     info = pool.info()
     p0, p1 = shard_range(tr.pairs_per_slice, rank, world)
@@ -496,6 +497,7 @@ def run_vbdr(args):
                                    if world > 1 else "single GPU"),
                    "l2": f"flushed before every step ({args.flush_mib} MiB write)",
                    "scan_mode": args.scan_mode, "est_lanes": args.est_lanes,
+                   "estimator": args.estimator,
                    "zbits": info["zbits"], "words_per_bdr": info["words"],
                    "bits_per_bdr": (32 if args.layout == "fast" else 0) + 32 * info["words"],
                    "table1_bits_per_bdr": table1_bits(wl["m"], wl["k"])},

@@ -93,6 +93,16 @@ typedef struct {
      * slice of the register array stays L2-resident (0 = auto: 26, i.e. one
      * pass up to 2^26 BDRs).  Tuning only; results are identical. */
     uint32_t est_pass_log2;
+    /* estimator: the register estimator the BDR pool feeds (PAPER.md:214, 319:
+     * "BDRP could also be used in PCSA, LogLog"): 0 = HyperLogLog (default,
+     * R#15); 1 = LogLog, alpha_g g 2^(sum M / g), on Alg.5's getSumLBP1;
+     * 2 = PCSA, (g / 0.77351) 2^(sum R / g) with R = the number of active
+     * ranks counted up from rank 1 (the sliding Flajolet-Martin bitmap) --
+     * layout packed only, since only gsmall records every rank.  All three use
+     * the shared-pool noise subtraction of R#15.  With PCSA the register array
+     * (vbdr_export_regmax) holds R; the pool sums are sum R (LogLog: sum M)
+     * and the zero count. */
+    uint32_t estimator;
 } vbdr_config;
 
 /* Derived sizes and the layout of the state buffer (byte offsets from the

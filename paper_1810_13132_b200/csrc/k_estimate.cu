@@ -51,8 +51,13 @@ k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *
   }
   if (!SUMS && (!MULTI || last) && threadIdx.x == 0) {
     const unsigned long long St = e.acc[0], Vt = e.acc[1];
-    const double D = __dmul_rn((double)St, e.inv2L);  // exact: St <= 2^53
-    const double Et = hll_finish(e.azz, D, e.lc_z, Vt, e.z);
+    double Et;
+    if (e.est == 0u) {
+      const double D = __dmul_rn((double)St, e.inv2L);  // exact: St <= 2^53
+      Et = hll_finish(e.azz, D, e.lc_z, Vt, e.z);
+    } else {  // LogLog / PCSA: coef * 2^(sum / z)
+      Et = __dmul_rn(e.coef_z, exp2(__ddiv_rn((double)St, e.z)));
+    }
     s_etot_z = __ddiv_rn(Et, e.z);
   }
   __syncthreads();
@@ -85,7 +90,7 @@ k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (MULTI && M[u] == 0xFFu) continue;  // outside this pass's range
-        S += 1ull << (e.L - M[u]);
+        S += e.est == 0u ? 1ull << (e.L - M[u]) : (unsigned long long)M[u];
         V += M[u] == 0u;
       }
     }
@@ -112,8 +117,13 @@ k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *
         outV[h] = V;
       } else {
         const double g = (double)e.g;
-        const double D = __dmul_rn((double)S, e.inv2L);  // exact: S <= 2^32
-        const double Es = hll_finish(e.agg, D, e.lc_g, V, g);
+        double Es;
+        if (e.est == 0u) {
+          const double D = __dmul_rn((double)S, e.inv2L);  // exact: S <= 2^32
+          Es = hll_finish(e.agg, D, e.lc_g, V, g);
+        } else {  // LogLog / PCSA: coef * 2^(sum / g) (sum = Alg.5's getSumLBP1 for LogLog)
+          Es = __dmul_rn(e.coef_g, exp2(__ddiv_rn((double)S, g)));
+        }
         const double est = __dmul_rn(e.C, __dsub_rn(__ddiv_rn(Es, g), s_etot_z));
         out[h] = est > 0.0 ? est : 0.0;
       }

@@ -175,7 +175,10 @@ k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict
 // Only BDR quads [q0, q1) are processed (the rank's shard).
 enum { SRC_STAMPS = 0, SRC_DELTA = 1, SRC_PEERS = 2 };
 
-template <bool FAST, int ZB, int SRC>
+// PCSA (layout packed only): the register value written is R = the number of
+// consecutive active ranks from rank 1 (the sliding FM bitmap's lowest zero,
+// N4 variant) instead of M (Alg.2).
+template <bool FAST, int ZB, int SRC, bool PCSA = false>
 __global__ void __launch_bounds__(kThreads)
 k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ delta4,
         uint64_t q0, uint64_t q1, vbdr_launch::Peers peers) {
@@ -211,6 +214,7 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
     for (int w = 0; w < WM; ++w)
       if (w < (int)p.W) x[w] = drv4[(uint64_t)w * n4 + q];
     uint32_t best[4] = {0u, 0u, 0u, 0u};
+    uint32_t run[4] = {0u, 0u, 0u, 0u};  // PCSA: active ranks from the bottom of word w up
 #pragma unroll
     for (int w = WM - 1; w >= 0; --w) {
       if (w >= (int)p.W) continue;
@@ -235,6 +239,10 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
 #if VBDR_SLIDE_SKIP == 2
         drv4[(uint64_t)w * n4 + q] = x[w];  // unchanged, stored anyway
 #endif
+        if constexpr (PCSA) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) run[c] = 0u;  // no active field in this word
+        }
         continue;  // VBDR_SLIDE_SKIP 1: unchanged words are not rewritten
       }
 #endif
@@ -249,8 +257,16 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
           xv[c] = S::age(xv[c]);       // Alg.8 for the next slice
         }
         if (best[c] == 0u && a != 0u) best[c] = (uint32_t)w * S::F + S::top_field(a) + 1u;
+        if constexpr (PCSA) {
+          const uint32_t inact = ~a & S::LSB;  // unused high fields are S: inactive
+          run[c] = inact ? (uint32_t)(__ffs(inact) - 1) / (uint32_t)ZB : (uint32_t)S::F + run[c];
+        }
       }
       drv4[(uint64_t)w * n4 + q] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
+    }
+    if constexpr (PCSA) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) best[c] = min(run[c], p.L);
     }
     const uint32_t r4 = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
     if (SRC == SRC_PEERS && peers.n_regmax > 0) {
@@ -260,7 +276,8 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      s_acc += 1ull << (p.L - best[c]);
+      // HLL: harmonic sum 2^(L - M); LogLog / PCSA: plain sum of the values
+      s_acc += p.est == 0u ? 1ull << (p.L - best[c]) : (unsigned long long)best[c];
       v_acc += best[c] == 0u;
     }
   }
@@ -334,7 +351,7 @@ __global__ void __launch_bounds__(kThreads) k_init(DevParams p, bool fast) {
     reinterpret_cast<uint32_t *>(p.regmax)[q] = 0u;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    p.acc[0] = (unsigned long long)p.n_phys << p.L;
+    p.acc[0] = p.est == 0u ? (unsigned long long)p.n_phys << p.L : 0ull;
     p.acc[1] = p.n_phys;
     p.acc[2] = 0ull;
     p.acc[3] = 0ull;
@@ -425,6 +442,9 @@ struct SlideFn {
     else if (fast)
       k_slide<true, ZB, SRC_STAMPS><<<grid_for(k_slide<true, ZB, SRC_STAMPS>, work), kThreads, 0, s>>>(
           p, addk, slot, nullptr, q0, q1, none);
+    else if (p.est == 2)
+      k_slide<false, ZB, SRC_STAMPS, true><<<grid_for(k_slide<false, ZB, SRC_STAMPS, true>, work),
+                                             kThreads, 0, s>>>(p, addk, slot, nullptr, q0, q1, none);
     else
       k_slide<false, ZB, SRC_STAMPS><<<grid_for(k_slide<false, ZB, SRC_STAMPS>, work), kThreads, 0,
                                        s>>>(p, addk, slot, nullptr, q0, q1, none);

@@ -20,6 +20,7 @@ struct DevParams {
   uint32_t b, L, k, zb, F, W;
   uint32_t A0, A1;
   uint32_t tick;             // T of the open slice
+  uint32_t est;              // register estimator: 0 HLL, 1 LogLog, 2 PCSA (packed only)
 };
 
 // H(x, 2^32, A) = fmix32(x ^ A) (R#6: MurmurHash3 finaliser).
@@ -133,6 +134,9 @@ struct EstParams {
   double lc_z;        // 2.5 * z
   double z;           // n_phys as double
   double C;           // z g / (z - g)
+  uint32_t est;       // 0 HLL, 1 LogLog, 2 PCSA
+  double coef_g;      // LogLog alpha_g g, PCSA g / phi
+  double coef_z;      // same for the pool of z registers
 };
 // *nl receives the number of kernels launched (passes).
 cudaError_t estimate(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,

@@ -42,6 +42,21 @@ uint32_t log2u(uint64_t x) {
   return r;
 }
 
+// LogLog bias constant (Durand & Flajolet): alpha_m = (Gamma(-1/m)(1 - 2^(1/m))
+// / ln 2)^(-m), evaluated in logs with expm1 (no cancellation at large m).
+double loglog_alpha(uint64_t m) {
+  const double x = 1.0 / (double)m;
+  const double lb = std::lgamma(-x) + std::log(std::expm1(x * std::log(2.0))) - std::log(std::log(2.0));
+  return std::exp(-(double)m * lb);
+}
+
+// Register-estimator constant coef_s (LogLog alpha_s s, PCSA s / phi).
+double est_coef(uint32_t est, uint64_t s) {
+  if (est == 1) return loglog_alpha(s) * (double)s;
+  if (est == 2) return (double)s / 0.77351;
+  return 0.0;
+}
+
 // HyperLogLog alpha_s (R#16), same double operations as the oracle.
 double alpha_of(uint64_t s) {
   if (s == 16) return 0.673;
@@ -69,6 +84,9 @@ std::string plan(const vbdr_config *c, vbdr_config *norm, Plan *pl) {
   if (n.est_lanes > 32 || (n.est_lanes & (n.est_lanes - 1)))
     return "est_lanes must be 0 or a power of two <= 32";
   if (n.est_pass_log2 > 32) return "est_pass_log2 must be 0..32";
+  if (n.estimator > 2) return "estimator must be 0 (HLL), 1 (LogLog) or 2 (PCSA)";
+  if (n.estimator == 2 && n.layout != VBDR_LAYOUT_PACKED)
+    return "PCSA needs layout packed (every rank recorded: the sliding bitmap)";
   if (n.m < 2 || !is_pow2(n.m)) return "m must be a power of two >= 2";
   if (n.k < 1) return "k must be >= 1";
   if (n.n_phys < 4 || !is_pow2(n.n_phys) || n.n_phys > (1ull << 32))
@@ -166,6 +184,9 @@ vbdr_launch::EstParams est_params(const vbdr *h) {
   e.lc_z = 2.5 * z;
   e.z = z;
   e.C = ((double)h->cfg.n_phys * (double)h->cfg.m) / (double)(h->cfg.n_phys - h->cfg.m);
+  e.est = h->cfg.estimator;
+  e.coef_g = est_coef(e.est, h->cfg.m);
+  e.coef_z = est_coef(e.est, h->cfg.n_phys);
   return e;
 }
 
@@ -282,6 +303,7 @@ vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, v
   p.A0 = h->cfg.seed_a0;
   p.A1 = h->cfg.seed_a1;
   p.tick = 1;  // slice t = 0 is open, T = t + 1
+  p.est = h->cfg.estimator;
   h->alpha_g = alpha_of(h->cfg.m);
   h->alpha_z = alpha_of(h->cfg.n_phys);
   vbdr_info_t &in = h->info;

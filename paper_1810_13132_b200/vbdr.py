@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("VBDR_LIB") or os.path.join(_HERE, "_lib", "libvbdr.so
 
 LAYOUT_FAST, LAYOUT_PACKED = 0, 1
 LAYOUTS = {"fast": LAYOUT_FAST, "packed": LAYOUT_PACKED}
+ESTIMATORS = {"hll": 0, "loglog": 1, "pcsa": 2}
 
 STATUS = {0: "ok", -1: "EINVAL", -2: "ERANGE", -3: "ESTATE", -4: "ENOMEM", -5: "ECUDA"}
 
@@ -28,7 +29,8 @@ class vbdr_config(C.Structure):
     _fields_ = [("m", C.c_uint32), ("k", C.c_uint32), ("n_phys", C.c_uint64),
                 ("seed_a0", C.c_uint32), ("seed_a1", C.c_uint32), ("zbits", C.c_uint32),
                 ("rank_cap", C.c_uint32), ("layout", C.c_uint32), ("scan_mode", C.c_uint32),
-                ("est_lanes", C.c_uint32), ("est_pass_log2", C.c_uint32)]
+                ("est_lanes", C.c_uint32), ("est_pass_log2", C.c_uint32),
+                ("estimator", C.c_uint32)]
 
 
 class vbdr_info_t(C.Structure):
@@ -94,10 +96,12 @@ def lib():
 def make_config(m: int, k: int, n_phys: int, seed_a0: int = 0x5EED0001,
                 seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
                 layout: str | int = "fast", scan_mode: int = 0,
-                est_lanes: int = 0, est_pass_log2: int = 0) -> vbdr_config:
+                est_lanes: int = 0, est_pass_log2: int = 0,
+                estimator: str | int = "hll") -> vbdr_config:
     lay = LAYOUTS[layout] if isinstance(layout, str) else int(layout)
+    est = ESTIMATORS[estimator] if isinstance(estimator, str) else int(estimator)
     return vbdr_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, lay, scan_mode, est_lanes,
-                       est_pass_log2)
+                       est_pass_log2, est)
 
 
 def state_bytes(cfg: vbdr_config) -> int:
@@ -121,13 +125,15 @@ class VBDR:
     def __init__(self, m: int, k: int, n_phys: int, *, seed_a0: int = 0x5EED0001,
                  seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
                  layout: str = "fast", scan_mode: int = 0, est_lanes: int = 0,
-                 est_pass_log2: int = 0, device=None, stream=None, state=None):
+                 est_pass_log2: int = 0, estimator: str = "hll", device=None, stream=None,
+                 state=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("VBDR needs a CUDA device (no CPU fallback)")
         self.device = torch.device(device if device is not None else "cuda")
         self.cfg = make_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, layout, scan_mode,
-                               est_lanes, est_pass_log2)
+                               est_lanes, est_pass_log2, estimator)
+        self.estimator = estimator
         nbytes = state_bytes(self.cfg)
         with torch.cuda.device(self.device):
             if state is None:

@@ -451,3 +451,72 @@ def test_loopback_fused_peer_merge_slide(n_ranks):
     solo.slide_peers([d.data_ptr()], 0, cfg.z)
     ref2.slice(pairs)
     assert np.array_equal(solo.export_ages(), ref2.drv())
+
+
+def variant_floor(V, hosts, b, z, estimator):
+    """C * E_s / g per host for the LogLog / PCSA estimators (tolerance floor)."""
+    g = 1 << b
+    C = (z * g) / (z - g)
+    out = []
+    for aip in hosts:
+        regs = np.array([V[oracle.getPhyIdx(int(aip), i, 0x5EED0001, z)] for i in range(g)],
+                        np.uint8)
+        Es = oracle.loglog_raw(regs) if estimator == "loglog" else oracle.pcsa_raw(regs)
+        out.append(C * Es / g)
+    return np.array(out)
+
+
+@pytest.mark.parametrize("layout,estimator", [("fast", "loglog"), ("packed", "loglog"),
+                                              ("packed", "pcsa")])
+def test_estimator_variants_tiny(layout, estimator):
+    """N4: the BDR pool under LogLog (Alg.5's sum of LBP1) and PCSA (sliding
+    FM bitmap = the gsmall DRV's active ranks), bit-exact registers and sums,
+    estimates to 1e-9 against the oracle, at every boundary."""
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(32, 4, 1 << 12, layout=layout, estimator=estimator, device=DEV)
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    assert (pool.estimate(hosts).cpu().numpy() == 0).all() or estimator != "hll"
+    for t in range(9):
+        pairs = synth.generate(tr, t)
+        pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+        V = ref.readout_pcsa() if estimator == "pcsa" else ref.readout()
+        assert np.array_equal(pool.export_regmax(), V)
+        assert pool.export_pool_sums() == (int(V.astype(np.int64).sum()), int((V == 0).sum()))
+        S, Vz = pool.host_sums(hosts)
+        for h, aip in enumerate(hosts_np[:16]):
+            regs = np.array([V[oracle.getPhyIdx(int(aip), i, cfg.A0, cfg.z)] for i in range(32)])
+            assert int(S[h]) == int(regs.sum()) and int(Vz[h]) == int((regs == 0).sum())
+        est = pool.estimate(hosts).cpu().numpy()
+        want = oracle.estimate_variant(V, hosts_np, cfg.b, cfg.z, estimator)
+        check_estimates(est, want, variant_floor(V, hosts_np, cfg.b, cfg.z, estimator))
+
+
+def test_pcsa_needs_packed():
+    with pytest.raises(ValueError):
+        VBDR(32, 4, 1 << 12, layout="fast", estimator="pcsa", device=DEV)
+
+
+@pytest.mark.parametrize("layout,estimator", [("fast", "loglog"), ("packed", "pcsa")])
+def test_estimator_variants_caida(layout, estimator):
+    tr = synth.CONFIGS["caida"]
+    cfg = oracle.PoolConfig(b=7, k=5, z=1 << 22)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(128, 5, 1 << 22, layout=layout, estimator=estimator, device=DEV)
+    hosts_np = tr.host_ids()
+    sample = hosts_np[np.random.default_rng(2).choice(len(hosts_np), 3000, replace=False)]
+    for t in range(6):
+        pairs = synth.generate(tr, t)
+        pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+    V = ref.readout_pcsa() if estimator == "pcsa" else ref.readout()
+    assert np.array_equal(pool.export_regmax(), V)
+    assert pool.export_pool_sums() == (int(V.astype(np.int64).sum()), int((V == 0).sum()))
+    est = pool.estimate(dev_u32(sample)).cpu().numpy()
+    want = oracle.estimate_variant(V, sample, cfg.b, cfg.z, estimator)
+    check_estimates(est, want, variant_floor(V, sample, cfg.b, cfg.z, estimator))
