@@ -520,3 +520,29 @@ def test_estimator_variants_caida(layout, estimator):
     est = pool.estimate(dev_u32(sample)).cpu().numpy()
     want = oracle.estimate_variant(V, sample, cfg.b, cfg.z, estimator)
     check_estimates(est, want, variant_floor(V, sample, cfg.b, cfg.z, estimator))
+
+
+@pytest.mark.parametrize("layout", ["fast", "packed"])
+@pytest.mark.parametrize("m,n_phys,k,zbits,rank_cap", [(1 << 14, 1 << 16, 3, 0, 0),
+                                                      (64, 1 << 12, 4, 5, 9),
+                                                      (4, 1 << 8, 2, 0, 1)])
+def test_unusual_configs(layout, m, n_phys, k, zbits, rank_cap):
+    """Huge virtual vectors (g = 2^14 > the shared s1 table), explicit wide DRs,
+    a rank cap (R#3: rho = min(rho, L)), and L = 1."""
+    b = m.bit_length() - 1
+    cfg = oracle.PoolConfig(b=b, k=k, z=n_phys, zb=zbits, L=rank_cap)
+    if layout == "packed" and zbits == 0 and (1 << cfg.zb) - 2 < k:
+        cfg = oracle.PoolConfig(b=b, k=k, z=n_phys, zb=cfg.zb + 1, L=rank_cap)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(m, k, n_phys, layout=layout, zbits=zbits, rank_cap=rank_cap, device=DEV)
+    tr = synth.TraceConfig("odd", hosts=300, pairs_per_slice=5001, U0=5000, seed=m + k)
+    hosts_np = tr.host_ids()
+    slices = []
+    for t in range(k + 3):
+        pairs = synth.generate(tr, t)
+        slices.append(pairs)
+        pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+    compare_boundary(pool, ref, [], hosts_np, dev_u32(hosts_np),
+                     np.concatenate(slices[-k:]))
