@@ -203,6 +203,43 @@ vbdr_status vbdr_estimate(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
 vbdr_status vbdr_host_sums(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
                            uint64_t *d_S, uint32_t *d_V, void *stream);
 
+/* ---- plan-based estimation (a fixed host list, pools up to 2^22 BDRs) -- */
+
+/* The gather estimate reads each register with its own L2 sector request.  A
+ * PLAN preprocesses a host list once: every (host, i) gather of Alg.5 is
+ * precomputed and grouped by 64 KB block of the register array; per slice the
+ * estimate then streams the array block by block through shared memory (TMA
+ * bulk copies) and every thread adds its hosts' registers from there.  Same
+ * integer sums, same fp64 finish: results are bit-identical to
+ * vbdr_estimate.  Needs n_phys in [64, 2^22] and n_hosts <= 7 * 512 * SMs
+ * (530k on B200); otherwise VBDR_ERANGE. */
+
+/* SYNC, host only.  Bytes of the caller's plan buffer for n_hosts hosts. */
+vbdr_status vbdr_plan_bytes(const vbdr_t *h, uint64_t n_hosts, uint64_t *bytes);
+
+/* SYNC.  Build the plan for d_hosts (u32[n_hosts], kept by the plan only as
+ * indices: later estimates report host j at position j) into d_plan
+ * (256-byte aligned, >= vbdr_plan_bytes).  VBDR_ERANGE if a register block
+ * would hold more entries than one shared-memory stage (then use
+ * vbdr_estimate).  The plan belongs to this handle and stays valid until
+ * vbdr_plan_release or the handle is destroyed. */
+vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, void *d_plan,
+                            uint64_t bytes, void *stream);
+
+/* vbdr_estimate for the plan's hosts (d_out f64[n_hosts]). */
+vbdr_status vbdr_estimate_plan(vbdr_t *h, const void *d_plan, double *d_out, void *stream);
+
+/* vbdr_host_sums for the plan's hosts. */
+vbdr_status vbdr_host_sums_plan(vbdr_t *h, const void *d_plan, uint64_t *d_S, uint32_t *d_V,
+                                void *stream);
+
+/* SYNC.  VBDR_ECUDA if a plan estimate on this plan ever timed out waiting for
+ * a staged transfer (never expected; the kernel stops instead of hanging). */
+vbdr_status vbdr_plan_check(vbdr_t *h, const void *d_plan, void *stream);
+
+/* Forget a plan (the caller frees its buffer). */
+vbdr_status vbdr_plan_release(vbdr_t *h, const void *d_plan);
+
 /* ---- host-buffer entry points (end-to-end path) ---------------------- */
 
 /* vbdr_scan_slice on HOST pairs: copies h_pairs (pinned for overlap) through

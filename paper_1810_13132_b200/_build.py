@@ -30,6 +30,7 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptx
 SOURCES = [
     ("k_scan_slide.cu", []),
     ("k_estimate.cu", ["-fmad=false"]),
+    ("k_plan.cu", ["-fmad=false"]),
     ("vbdr_host.cu", []),
 ]
 

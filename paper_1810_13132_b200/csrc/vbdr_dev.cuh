@@ -138,6 +138,27 @@ struct EstParams {
   double coef_g;      // LogLog alpha_g g, PCSA g / phi
   double coef_z;      // same for the pool of z registers
 };
+// Plan-based estimate (k_plan.cu): a host list preprocessed into per-(CTA,
+// register block) entry runs.  Layout of the caller's plan buffer.
+constexpr int kPlanThreads = 512;
+constexpr int kPlanSlots = 7;     // hosts per thread
+constexpr int kPlanEntCap = 8192; // entries per (CTA, block) staged in shared memory
+struct PlanLayout {
+  uint32_t ctas, phases, block_log2;
+  uint64_t n_hosts;
+  uint32_t *range_base;  // [ctas * phases + 1]
+  uint32_t *starts;      // [ctas * phases * (kPlanThreads + 4)]
+  uint32_t *counts;      // [ctas * phases * kPlanThreads] (build scratch)
+  uint32_t *range_size;  // [ctas * phases] (build scratch)
+  uint32_t *entries;
+  uint32_t *max_range;   // build: largest (CTA, block) entry count
+  unsigned long long *error;  // estimate: set if a staged transfer never landed
+};
+cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, uint32_t g,
+                       uint32_t A0, uint32_t mask, uint32_t *range_size_scratch, cudaStream_t s);
+cudaError_t estimate_plan(const EstParams &e, const PlanLayout &pl, uint64_t n, double *out,
+                          unsigned long long *outS, uint32_t *outV, cudaStream_t s);
+
 // *nl receives the number of kernels launched (passes).
 cudaError_t estimate(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
                      unsigned long long *outS, uint32_t *outV, cudaStream_t s, uint32_t *nl);

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -24,6 +25,7 @@ struct vbdr {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_scanned[2] = {nullptr, nullptr};
+  std::map<const void *, vbdr_launch::PlanLayout> plans;  // built plans by device address
   cudaEvent_t ev_hosts_in = nullptr;    // host ids copied (copy stream)
   cudaEvent_t ev_hosts_free = nullptr;  // last estimate that read the host stage
 };
@@ -206,6 +208,60 @@ void decode_ages(const vbdr *h, WordAt word, int mode, uint16_t *out) {
     }
     out[r - 1] = (uint16_t)v;
   }
+}
+
+// Plan geometry for this pool: blocks of up to 2^16 registers (64 KB in shared
+// memory), one persistent CTA per SM.
+struct PlanGeom {
+  uint32_t ctas, phases, block_log2;
+  uint64_t nkeys, off_range_base, off_starts, off_counts, off_range_size, off_misc, off_entries,
+      bytes;
+};
+
+bool plan_geom(const vbdr *h, uint64_t n_hosts, PlanGeom *g) {
+  const uint64_t z = h->p.n_phys;
+  if (z < 64 || z > (1ull << 22)) return false;  // the array streams through shared memory
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms <= 0) sms = 148;
+  const uint64_t T = (uint64_t)sms * vbdr_launch::kPlanThreads;
+  if (n_hosts == 0 || n_hosts > T * vbdr_launch::kPlanSlots) return false;
+  g->ctas = (uint32_t)sms;
+  g->block_log2 = z >= (1ull << 16) ? 16u : (uint32_t)log2u(z);
+  g->phases = (uint32_t)(z >> g->block_log2);
+  g->nkeys = (uint64_t)g->ctas * g->phases;
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) {
+    const uint64_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  g->off_range_base = take(4 * (g->nkeys + 1));
+  g->off_starts = take(4 * g->nkeys * (vbdr_launch::kPlanThreads + 4));
+  g->off_counts = take(4 * g->nkeys * vbdr_launch::kPlanThreads);
+  g->off_range_size = take(4 * g->nkeys);
+  g->off_misc = take(64);
+  g->off_entries = take(4 * (n_hosts * h->cfg.m + 4 * g->nkeys));
+  g->bytes = off;
+  return true;
+}
+
+vbdr_launch::PlanLayout plan_layout(const PlanGeom &g, void *d_plan, uint64_t n_hosts) {
+  uint8_t *b = static_cast<uint8_t *>(d_plan);
+  vbdr_launch::PlanLayout pl{};
+  pl.ctas = g.ctas;
+  pl.phases = g.phases;
+  pl.block_log2 = g.block_log2;
+  pl.n_hosts = n_hosts;
+  pl.range_base = reinterpret_cast<uint32_t *>(b + g.off_range_base);
+  pl.starts = reinterpret_cast<uint32_t *>(b + g.off_starts);
+  pl.counts = reinterpret_cast<uint32_t *>(b + g.off_counts);
+  pl.range_size = reinterpret_cast<uint32_t *>(b + g.off_range_size);
+  pl.max_range = reinterpret_cast<uint32_t *>(b + g.off_misc);
+  pl.error = reinterpret_cast<unsigned long long *>(b + g.off_misc + 8);
+  pl.entries = reinterpret_cast<uint32_t *>(b + g.off_entries);
+  return pl;
 }
 
 vbdr_status ensure_pipeline(vbdr *h, cudaStream_t cs) {
@@ -436,6 +492,86 @@ vbdr_status vbdr_slide_peers(vbdr_t *h, const uint8_t *const *h_peer_delta, uint
   const cudaError_t e = vbdr_launch::slide_peers(h->p, pe, j0, j1, S(stream));
   if (e != cudaSuccess) return cuda_fail(h, e, "slide_peers launch");
   return after_slide(h, stream);
+}
+
+vbdr_status vbdr_plan_bytes(const vbdr_t *h, uint64_t n_hosts, uint64_t *bytes) {
+  if (!h || !bytes) return VBDR_EINVAL;
+  PlanGeom g;
+  *bytes = 0;
+  if (!plan_geom(h, n_hosts, &g)) return VBDR_ERANGE;
+  *bytes = g.bytes;
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, void *d_plan,
+                            uint64_t bytes, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  PlanGeom g;
+  if (!plan_geom(h, n_hosts, &g)) return fail(h, VBDR_ERANGE, "no plan for this pool / host count");
+  if (!d_hosts || !d_plan || (reinterpret_cast<uintptr_t>(d_plan) & 255u))
+    return fail(h, VBDR_EINVAL, "d_hosts and a 256-byte aligned d_plan are required");
+  if (bytes < g.bytes) return fail(h, VBDR_ENOMEM, "plan buffer too small");
+  if (vbdr_status s = check_async(h, "before plan_build")) return s;
+  const vbdr_launch::PlanLayout pl = plan_layout(g, d_plan, n_hosts);
+  cudaStream_t cs = S(stream);
+  cudaError_t e = vbdr_launch::plan_build(pl, d_hosts, n_hosts, h->cfg.m, h->p.A0, h->p.mask,
+                                          pl.range_size, cs);
+  uint32_t max_range = 0;
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(&max_range, pl.max_range, 4, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return cuda_fail(h, e, "plan_build");
+  h->info.launches += 4;
+  if (max_range > (uint32_t)vbdr_launch::kPlanEntCap) {
+    h->plans.erase(d_plan);
+    return fail(h, VBDR_ERANGE, "a register block holds more entries than shared memory stages");
+  }
+  h->plans[d_plan] = pl;
+  return VBDR_OK;
+}
+
+static vbdr_status estimate_with_plan(vbdr_t *h, const void *d_plan, double *d_out, uint64_t *d_S,
+                                      uint32_t *d_V, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  auto it = h->plans.find(d_plan);
+  if (it == h->plans.end()) return fail(h, VBDR_EINVAL, "unknown plan (build it with this handle)");
+  if (vbdr_status s = check_async(h, "before estimate_plan")) return s;
+  const cudaError_t e = vbdr_launch::estimate_plan(
+      est_params(h), it->second, it->second.n_hosts, d_out,
+      reinterpret_cast<unsigned long long *>(d_S), d_V, S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "estimate_plan launch");
+  h->info.launches += 1;
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_estimate_plan(vbdr_t *h, const void *d_plan, double *d_out, void *stream) {
+  if (!d_out) return fail(h, VBDR_EINVAL, "null d_out");
+  return estimate_with_plan(h, d_plan, d_out, nullptr, nullptr, stream);
+}
+
+vbdr_status vbdr_host_sums_plan(vbdr_t *h, const void *d_plan, uint64_t *d_S, uint32_t *d_V,
+                                void *stream) {
+  if (!d_S || !d_V) return fail(h, VBDR_EINVAL, "null d_S / d_V");
+  return estimate_with_plan(h, d_plan, nullptr, d_S, d_V, stream);
+}
+
+vbdr_status vbdr_plan_check(vbdr_t *h, const void *d_plan, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  auto it = h->plans.find(d_plan);
+  if (it == h->plans.end()) return fail(h, VBDR_EINVAL, "unknown plan");
+  unsigned long long err = 0;
+  cudaStream_t cs = S(stream);
+  cudaError_t e = cudaMemcpyAsync(&err, it->second.error, 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return cuda_fail(h, e, "plan_check");
+  if (err) return fail(h, VBDR_ECUDA, "a staged plan transfer timed out");
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_plan_release(vbdr_t *h, const void *d_plan) {
+  if (!h) return VBDR_EINVAL;
+  h->plans.erase(d_plan);
+  return VBDR_OK;
 }
 
 vbdr_status vbdr_estimate(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, double *d_out,

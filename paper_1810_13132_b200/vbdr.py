@@ -76,6 +76,12 @@ def lib():
             "vbdr_stamp_delta": [vp, vp, vp],
             "vbdr_debug_set_tick": [vp, u32],
             "vbdr_slide_peers": [vp, vp, u32, u64, u64, vp, vp, vp],
+            "vbdr_plan_bytes": [vp, u64, C.POINTER(u64)],
+            "vbdr_plan_build": [vp, vp, u64, vp, u64, vp],
+            "vbdr_estimate_plan": [vp, vp, vp, vp],
+            "vbdr_host_sums_plan": [vp, vp, vp, vp, vp],
+            "vbdr_plan_check": [vp, vp, vp],
+            "vbdr_plan_release": [vp, vp],
             "vbdr_slide_delta": [vp, vp, u64, u64, vp],
             "vbdr_export_ages_at": [vp, vp, u64, vp, vp, C.c_int, vp],
             "vbdr_export_regmax": [vp, vp, vp],
@@ -257,6 +263,49 @@ class VBDR:
                     "vbdr_estimate")
         return out
 
+    # ---------------------------------------------------- plan-based estimate
+    def plan(self, hosts, stream=None):
+        """``vbdr_plan_bytes`` + ``vbdr_plan_build``: preprocess a fixed host
+        list (device u32/int32 tensor) for repeated estimates.  Returns an
+        :class:`EstimatePlan`; raises ValueError when the pool or host count has
+        no plan (use :meth:`estimate`)."""
+        import torch
+        n = hosts.numel()
+        nbytes = C.c_uint64()
+        rc = lib().vbdr_plan_bytes(self._h, n, C.byref(nbytes))
+        if rc != 0:
+            raise ValueError(f"no estimate plan for n_phys={self.n_phys}, {n} hosts")
+        buf = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
+        rc = lib().vbdr_plan_build(self._h, C.c_void_p(hosts.data_ptr()), n,
+                                   C.c_void_p(buf.data_ptr()), nbytes.value, _stream_ptr(stream))
+        if rc == -2:  # ERANGE: a block overflows the shared-memory stage
+            raise ValueError(lib().vbdr_last_error(self._h).decode())
+        self._check(rc, "vbdr_plan_build")
+        return EstimatePlan(self, buf, n)
+
+    def estimate_plan(self, plan: "EstimatePlan", out=None, stream=None):
+        """``vbdr_estimate_plan``: estimates for the plan's hosts (float64)."""
+        import torch
+        if out is None:
+            out = torch.empty(plan.n_hosts, dtype=torch.float64, device=self.device)
+        self._check(lib().vbdr_estimate_plan(self._h, C.c_void_p(plan.buf.data_ptr()),
+                                             C.c_void_p(out.data_ptr()), _stream_ptr(stream)),
+                    "vbdr_estimate_plan")
+        return out
+
+    def host_sums_plan(self, plan: "EstimatePlan", stream=None):
+        import torch
+        S = torch.empty(plan.n_hosts, dtype=torch.int64, device=self.device)
+        V = torch.empty(plan.n_hosts, dtype=torch.int32, device=self.device)
+        self._check(lib().vbdr_host_sums_plan(self._h, C.c_void_p(plan.buf.data_ptr()),
+                                              C.c_void_p(S.data_ptr()), C.c_void_p(V.data_ptr()),
+                                              _stream_ptr(stream)), "vbdr_host_sums_plan")
+        return S, V
+
+    def plan_check(self, plan: "EstimatePlan", stream=None):
+        self._check(lib().vbdr_plan_check(self._h, C.c_void_p(plan.buf.data_ptr()),
+                                          _stream_ptr(stream)), "vbdr_plan_check")
+
     def host_sums(self, hosts, stream=None):
         """``vbdr_host_sums``: per host (S, V) of the integer stage."""
         import torch
@@ -324,6 +373,22 @@ class VBDR:
         self._check(lib().vbdr_export_pool_sums(self._h, C.byref(S), C.byref(V),
                                                 _stream_ptr(stream)), "vbdr_export_pool_sums")
         return S.value, V.value
+
+
+class EstimatePlan:
+    """A host list preprocessed by ``vbdr_plan_build`` (device buffer owned here)."""
+
+    def __init__(self, pool: VBDR, buf, n_hosts: int):
+        self.pool, self.buf, self.n_hosts = pool, buf, n_hosts
+
+    @property
+    def nbytes(self) -> int:
+        return self.buf.numel()
+
+    def release(self):
+        if self.buf is not None and getattr(self.pool, "_h", None):
+            lib().vbdr_plan_release(self.pool._h, C.c_void_p(self.buf.data_ptr()))
+        self.buf = None
 
 
 # ------------------------------------------------------------ multi-GPU plumbing

@@ -546,3 +546,59 @@ def test_unusual_configs(layout, m, n_phys, k, zbits, rank_cap):
         ref.slice(pairs)
     compare_boundary(pool, ref, [], hosts_np, dev_u32(hosts_np),
                      np.concatenate(slices[-k:]))
+
+
+@pytest.mark.parametrize("layout,estimator", [("fast", "hll"), ("packed", "hll"),
+                                              ("packed", "pcsa"), ("fast", "loglog")])
+def test_plan_estimate_tiny(layout, estimator):
+    """vbdr_estimate_plan: shared-memory-staged sums equal the gather kernel's
+    bit for bit and the oracle to 1e-9, at every boundary."""
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(32, 4, 1 << 12, layout=layout, estimator=estimator, device=DEV)
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    plan = pool.plan(hosts)
+    for t in range(7):
+        pairs = synth.generate(tr, t)
+        pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+        a = pool.estimate_plan(plan).cpu().numpy()
+        b = pool.estimate(hosts).cpu().numpy()
+        assert np.array_equal(a, b)
+        S1, V1 = pool.host_sums_plan(plan)
+        S2, V2 = pool.host_sums(hosts)
+        assert torch.equal(S1, S2) and torch.equal(V1, V2)
+        if estimator == "hll":
+            check_estimates(a, ref.estimate(ref.readout(), hosts_np),
+                            est_floor(ref, ref.readout(), hosts_np))
+    pool.plan_check(plan)
+
+
+def test_plan_estimate_caida_full_size():
+    """configs[1] at full size: the plan covers all 500k hosts of the bench."""
+    tr = synth.CONFIGS["caida"]
+    cfg = oracle.PoolConfig(b=7, k=5, z=1 << 22)
+    ref = oracle.Pool(cfg, "serial")
+    pool = VBDR(128, 5, 1 << 22, device=DEV)
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    plan = pool.plan(hosts)
+    for t in range(6):
+        pairs = synth.generate(tr, t)
+        pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+    a = pool.estimate_plan(plan).cpu().numpy()
+    assert np.array_equal(a, pool.estimate(hosts).cpu().numpy())
+    M = ref.readout()
+    check_estimates(a, ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
+    pool.plan_check(plan)
+
+
+def test_plan_refuses_large_pools():
+    pool = VBDR(256, 10, 1 << 23, device=DEV)
+    with pytest.raises(ValueError):
+        pool.plan(dev_u32(np.arange(10, dtype=np.uint32)))
