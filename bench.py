@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--scan-mode", type=int, default=0)
     ap.add_argument("--est-lanes", type=int, default=0)
     ap.add_argument("--estimator", default="hll", choices=["hll", "loglog", "pcsa"])
+    ap.add_argument("--estimate", default="auto", choices=["auto", "gather", "plan"],
+                    help="plan: shared-memory plan for the fixed host list (pools <= 2^22)")
     ap.add_argument("--merge", default="sharded", choices=["stamps", "delta", "sharded", "p2p"],
                     help="N>1 slide merge (paper_1810_13132_b200.slide_merged)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -301,6 +303,23 @@ def run_vbdr(args):
     hosts_all = tr.host_ids()
     hosts = torch.from_numpy(hosts_all[h0:h1].view(np.int32)).to(dev)
     est_out = torch.empty(h1 - h0, dtype=torch.float64, device=dev)
+    plan, plan_build_ms = None, None
+    if args.estimate in ("auto", "plan"):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        try:
+            plan = pool.plan(hosts)
+            plan_build_ms = (time.perf_counter() - t0) * 1e3
+        except ValueError:
+            if args.estimate == "plan":
+                raise
+            plan = None
+
+    def estimate(out):
+        if plan is not None:
+            pool.estimate_plan(plan, out=out)
+        else:
+            pool.estimate(hosts, out=out)
     flush = torch.empty(args.flush_mib << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     torch.cuda.synchronize()
@@ -361,7 +380,7 @@ def run_vbdr(args):
         pool.scan_slice(x)
         mark(evs, 1)
         close_slice(evs)
-        pool.estimate(hosts, out=est_out)
+        estimate(est_out)
         mark(evs, 5)
 
     # warm-up
@@ -412,7 +431,10 @@ def run_vbdr(args):
         def e2e_step(i):
             pool.scan_slice_host(h_inputs[i % len(h_inputs)], stage)
             close_slice()
-            pool.estimate_host(h_hosts, hstage, ostage, h_out)
+            if plan is not None:  # the host list lives in the plan (built once)
+                pool.estimate_plan_host(plan, ostage, h_out)
+            else:
+                pool.estimate_host(h_hosts, hstage, ostage, h_out)
 
         for i in range(3):
             e2e_step(i)
@@ -432,7 +454,8 @@ def run_vbdr(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t[0])
         e2e = {"value": round(tr.pairs_per_slice / (e2e_ms / args.steps * 1e-3) / 1e6, 3),
-               "unit": "Mpairs/s", "h2d_bytes_per_step": 8 * n_local * world + 4 * tr.hosts,
+               "unit": "Mpairs/s",
+               "h2d_bytes_per_step": 8 * n_local * world + (0 if plan is not None else 4 * tr.hosts),
                "d2h_bytes_per_step": 8 * tr.hosts,
                "ms_per_step": e2e_ms / args.steps,
                "timing": "one CUDA-event region over all steps, copies pipelined across steps"}
@@ -477,6 +500,20 @@ def run_vbdr(args):
                      "traffic": traffic.get("estimate"), "hosts": h1 - h0, "gathers": gathers,
                      "peak_source": f"random 1-byte LDG gather ceiling, {tab} table ({CEIL_SRC})"},
     }
+    if plan is not None:
+        # The plan path streams, per slice: 4 B of plan entry per gather, the
+        # run starts, the register array once per SM (from L2; counted once
+        # here as DRAM bytes), 8 B of estimate per host.
+        ctas = torch.cuda.get_device_properties(dev).multi_processor_count
+        phases = max(1, wl["n_phys"] >> 16)
+        plan_bytes = 4 * gathers + 4 * ctas * phases * 516 + wl["n_phys"] + 8 * (h1 - h0)
+        plan_gbs = plan_bytes / (kern["estimate"] * 1e-3) / 1e9
+        kernels["estimate"] = {
+            "ms": kern["estimate"], "path": "plan", "bound": "hbm", "achieved": round(plan_gbs, 1),
+            "peak": hbm, "unit": "GB/s", "frac": round(plan_gbs / hbm, 4),
+            "algorithmic_bytes": plan_bytes, "traffic": traffic.get("estimate_plan"),
+            "gathers_per_s": round(g_rate * 1e9), "hosts": h1 - h0, "gathers": gathers,
+            "peak_source": hbm_src}
     dominant = max(("scan", "slide", "estimate"), key=lambda n: kern[n])
     roof = {"kernel": dominant, **{k: v for k, v in kernels[dominant].items() if k != "ms"}}
 
@@ -498,6 +535,9 @@ def run_vbdr(args):
                    "l2": f"flushed before every step ({args.flush_mib} MiB write)",
                    "scan_mode": args.scan_mode, "est_lanes": args.est_lanes,
                    "estimator": args.estimator,
+                   "estimate_path": "plan" if plan is not None else "gather",
+                   "plan_build_ms": round(plan_build_ms, 2) if plan_build_ms else None,
+                   "plan_bytes": plan.nbytes if plan is not None else None,
                    "zbits": info["zbits"], "words_per_bdr": info["words"],
                    "bits_per_bdr": (32 if args.layout == "fast" else 0) + 32 * info["words"],
                    "table1_bits_per_bdr": table1_bits(wl["m"], wl["k"])},

@@ -229,6 +229,11 @@ vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts
 /* vbdr_estimate for the plan's hosts (d_out f64[n_hosts]). */
 vbdr_status vbdr_estimate_plan(vbdr_t *h, const void *d_plan, double *d_out, void *stream);
 
+/* vbdr_estimate_plan into the device stage d_out_stage, then copied to the
+ * HOST buffer h_out (pinned for overlap; valid after `stream` syncs). */
+vbdr_status vbdr_estimate_plan_host(vbdr_t *h, const void *d_plan, double *d_out_stage,
+                                    double *h_out, void *stream);
+
 /* vbdr_host_sums for the plan's hosts. */
 vbdr_status vbdr_host_sums_plan(vbdr_t *h, const void *d_plan, uint64_t *d_S, uint32_t *d_V,
                                 void *stream);

@@ -549,6 +549,17 @@ vbdr_status vbdr_estimate_plan(vbdr_t *h, const void *d_plan, double *d_out, voi
   return estimate_with_plan(h, d_plan, d_out, nullptr, nullptr, stream);
 }
 
+vbdr_status vbdr_estimate_plan_host(vbdr_t *h, const void *d_plan, double *d_out_stage,
+                                    double *h_out, void *stream) {
+  if (!h || !d_out_stage || !h_out) return VBDR_EINVAL;
+  if (vbdr_status s = estimate_with_plan(h, d_plan, d_out_stage, nullptr, nullptr, stream)) return s;
+  const uint64_t n = h->plans[d_plan].n_hosts;
+  const cudaError_t e =
+      cudaMemcpyAsync(h_out, d_out_stage, 8ull * n, cudaMemcpyDeviceToHost, S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "estimate_plan_host");
+  return VBDR_OK;
+}
+
 vbdr_status vbdr_host_sums_plan(vbdr_t *h, const void *d_plan, uint64_t *d_S, uint32_t *d_V,
                                 void *stream) {
   if (!d_S || !d_V) return fail(h, VBDR_EINVAL, "null d_S / d_V");

@@ -46,7 +46,9 @@ SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice",
            "vbdr_estimate", "vbdr_host_sums", "vbdr_scan_slice_host", "vbdr_estimate_host",
            "vbdr_info", "vbdr_export_ages", "vbdr_export_ages_at", "vbdr_export_regmax",
            "vbdr_export_pool_sums", "vbdr_stamp_delta", "vbdr_slide_delta", "vbdr_debug_set_tick",
-           "vbdr_slide_peers",
+           "vbdr_slide_peers", "vbdr_plan_bytes", "vbdr_plan_build", "vbdr_estimate_plan",
+           "vbdr_host_sums_plan", "vbdr_plan_check", "vbdr_plan_release",
+           "vbdr_estimate_plan_host",
            "vbdr_last_error", "vbdr_status_string")
 
 _lib = None
@@ -80,6 +82,7 @@ def lib():
             "vbdr_plan_build": [vp, vp, u64, vp, u64, vp],
             "vbdr_estimate_plan": [vp, vp, vp, vp],
             "vbdr_host_sums_plan": [vp, vp, vp, vp, vp],
+            "vbdr_estimate_plan_host": [vp, vp, vp, vp, vp],
             "vbdr_plan_check": [vp, vp, vp],
             "vbdr_plan_release": [vp, vp],
             "vbdr_slide_delta": [vp, vp, u64, u64, vp],
@@ -292,6 +295,13 @@ class VBDR:
                                              C.c_void_p(out.data_ptr()), _stream_ptr(stream)),
                     "vbdr_estimate_plan")
         return out
+
+    def estimate_plan_host(self, plan: "EstimatePlan", d_out_stage, h_out, stream=None):
+        """``vbdr_estimate_plan_host``: estimates copied into a (pinned) CPU tensor."""
+        self._check(lib().vbdr_estimate_plan_host(self._h, C.c_void_p(plan.buf.data_ptr()),
+                                                  C.c_void_p(d_out_stage.data_ptr()),
+                                                  C.c_void_p(h_out.data_ptr()),
+                                                  _stream_ptr(stream)), "vbdr_estimate_plan_host")
 
     def host_sums_plan(self, plan: "EstimatePlan", stream=None):
         import torch
