@@ -79,8 +79,9 @@ def traffic(rep, key_prefix):
     out = {}
     for r in rows:
         name = short(r[ki])
-        kind = "scan" if name.startswith("k_scan") else "slide" if name.startswith(
-            "k_slide") else "estimate" if name.startswith("k_estimate") else None
+        kind = ("scan" if name.startswith("k_scan") else "slide" if name.startswith("k_slide")
+                else "estimate_plan" if name.startswith("k_estimate_plan")
+                else "estimate" if name.startswith("k_estimate") else None)
         if kind:
             b = float(r[rd]) * scale[units[rd]] + float(r[wr]) * scale[units[wr]]
             out[f"{key_prefix}/{kind}"] = int(b)
