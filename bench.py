@@ -393,19 +393,28 @@ def run_vbdr(args):
     clocks = ClockSampler(local) if rank == 0 else None
     if clocks:
         clocks.wait_first()
+    # per-kernel breakdown: a first pass with events between the kernels
     events = [[E() for _ in range(6)] for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        step(args.warmup + i, events[i])
+    barrier()
+    ms = np.array([[ev[j].elapsed_time(ev[j + 1]) for j in range(5)] for ev in events])
+    ms_k = ms.mean(axis=0)  # scan, merge, slide, gather, estimate
+    per_kernel_local = np.array([ms_k[0], ms_k[1] + ms_k[3], ms_k[2], ms_k[4]])
+    # headline: events only around each step (nothing between its kernels)
+    step_ev = [(E(), E()) for _ in range(args.steps)]
     launches0 = pool.info()["launches"]
     barrier()
     for i in range(args.steps):
         flush.fill_(i & 0xFF)  # L2 flush (> 126 MB L2), outside the step events
-        step(args.warmup + i, events[i])
+        step_ev[i][0].record(stream)
+        step(args.warmup + args.steps + i)
+        step_ev[i][1].record(stream)
     barrier()
     launches = pool.info()["launches"] - launches0
-    ms = np.array([[ev[j].elapsed_time(ev[j + 1]) for j in range(5)] for ev in events])
-    step_ms_local = ms.sum(axis=1)
-    local_total = float(step_ms_local.sum())
-    ms_k = ms.mean(axis=0)  # scan, merge, slide, gather, estimate
-    per_kernel_local = np.array([ms_k[0], ms_k[1] + ms_k[3], ms_k[2], ms_k[4]])
+    local_total = float(sum(a.elapsed_time(b) for a, b in step_ev))
     if world > 1:
         t = torch.tensor([local_total, *per_kernel_local.tolist()], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(kThreads)
 k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *__restrict__ out,
            unsigned long long *__restrict__ outS, uint32_t *__restrict__ outV, uint32_t pass,
            bool last) {
+  pdl_wait();
   extern __shared__ uint32_t s1tab[];
   __shared__ double s_etot_z;  // E_tot / z
   if constexpr (SMEM) {
@@ -129,6 +130,7 @@ k_estimate(EstParams e, const uint32_t *__restrict__ hosts, uint64_t n, double *
       }
     }
   }
+  pdl_trigger();
 }
 
 int sm_count() {
@@ -159,9 +161,8 @@ cudaError_t run(const EstParams &e, const uint32_t *hosts, uint64_t n, double *o
     const uint64_t need = (n * G + kThreads - 1) / kThreads;
     const uint64_t grid = need < resident ? need : resident;
     for (uint32_t p = 0; p < passes; ++p) {
-      kern<<<(uint32_t)(grid ? grid : 1), kThreads, smem, s>>>(e, hosts, n, out, outS, outV, p,
-                                                              p + 1 == passes);
-      const cudaError_t err = cudaGetLastError();
+      const cudaError_t err = launch(kern, dim3((uint32_t)(grid ? grid : 1)), dim3(kThreads), smem,
+                                     s, e, hosts, n, out, outS, outV, p, p + 1 == passes);
       if (err != cudaSuccess) return err;
     }
     return cudaSuccess;
@@ -178,8 +179,8 @@ cudaError_t run(const EstParams &e, const uint32_t *hosts, uint64_t n, double *o
   const uint64_t resident = (uint64_t)per_sm * sm_count();
   const uint64_t need = (n * G + kThreads - 1) / kThreads;
   const uint64_t grid = need < resident ? need : resident;
-  kern<<<(uint32_t)(grid ? grid : 1), kThreads, smem, s>>>(e, hosts, n, out, outS, outV, 0u, true);
-  return cudaGetLastError();
+  return launch(kern, dim3((uint32_t)(grid ? grid : 1)), dim3(kThreads), smem, s, e, hosts, n, out,
+                outS, outV, 0u, true);
 }
 
 template <int G>

@@ -180,6 +180,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
                 unsigned long long *__restrict__ outS, uint32_t *__restrict__ outV,
                 unsigned long long *__restrict__ err) {
   constexpr uint32_t BLOCK = 1u << BLOCK_LOG2;
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t raw[];
   PlanSmem<BLOCK_LOG2> &sm = *reinterpret_cast<PlanSmem<BLOCK_LOG2> *>(raw);
   const int tid = threadIdx.x;
@@ -250,6 +251,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
     }
     __syncthreads();
   }
+  pdl_trigger();
   const uint64_t T = (uint64_t)gridDim.x * kT;
   const uint64_t t = (uint64_t)blockIdx.x * kT + tid;
   const double g = (double)e.g;
@@ -283,8 +285,7 @@ cudaError_t launch_est(const EstParams &e, const PlanLayout &pl, uint64_t n, dou
   auto kern = outS ? k_estimate_plan<BL, true> : k_estimate_plan<BL, false>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  kern<<<pl.ctas, kT, smem, s>>>(e, pl, n, out, outS, outV, pl.error);
-  return cudaGetLastError();
+  return launch(kern, dim3(pl.ctas), dim3(kT), smem, s, e, pl, n, out, outS, outV, pl.error);
 }
 
 }  // namespace

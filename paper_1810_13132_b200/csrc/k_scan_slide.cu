@@ -127,6 +127,7 @@ template <bool FAST, int ZB, int MODE>
 __global__ void __launch_bounds__(kThreads)
 k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict__ tail,
        DevParams p) {
+  pdl_wait();
   constexpr int UNROLL = 4;
   ScanCache *cache = nullptr;
   if constexpr (MODE == 5) {  // only this mode pays for the shared memory
@@ -155,6 +156,7 @@ k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict
   }
   if (tail != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
     record<FAST, ZB, MODE>(tail[0], tail[1], p, tickbits, cache);
+  pdl_trigger();  // this block's work is issued: let the next kernel launch
 }
 
 // ------------------------------------------------------------------ slide
@@ -182,6 +184,7 @@ template <bool FAST, int ZB, int SRC, bool PCSA = false>
 __global__ void __launch_bounds__(kThreads)
 k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ delta4,
         uint64_t q0, uint64_t q1, vbdr_launch::Peers peers) {
+  pdl_wait();
   using S = Swar<ZB>;
   constexpr int WM = WMax<ZB>::value;
   const uint64_t n4 = p.n_phys >> 2;
@@ -281,6 +284,7 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
       v_acc += best[c] == 0u;
     }
   }
+  pdl_trigger();
   // block reduction, one atomic per block (integers: order-independent)
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
@@ -434,21 +438,20 @@ struct SlideFn {
     const uint64_t work = q1 - q0;
     const vbdr_launch::Peers none{};
     if (fast && peers)
-      k_slide<true, ZB, SRC_PEERS><<<grid_for(k_slide<true, ZB, SRC_PEERS>, work), kThreads, 0, s>>>(
-          p, addk, slot, nullptr, q0, q1, *peers);
-    else if (fast && delta4)
-      k_slide<true, ZB, SRC_DELTA><<<grid_for(k_slide<true, ZB, SRC_DELTA>, work), kThreads, 0, s>>>(
-          p, addk, slot, delta4, q0, q1, none);
-    else if (fast)
-      k_slide<true, ZB, SRC_STAMPS><<<grid_for(k_slide<true, ZB, SRC_STAMPS>, work), kThreads, 0, s>>>(
-          p, addk, slot, nullptr, q0, q1, none);
-    else if (p.est == 2)
-      k_slide<false, ZB, SRC_STAMPS, true><<<grid_for(k_slide<false, ZB, SRC_STAMPS, true>, work),
-                                             kThreads, 0, s>>>(p, addk, slot, nullptr, q0, q1, none);
-    else
-      k_slide<false, ZB, SRC_STAMPS><<<grid_for(k_slide<false, ZB, SRC_STAMPS>, work), kThreads, 0,
-                                       s>>>(p, addk, slot, nullptr, q0, q1, none);
-    return cudaGetLastError();
+      return launch(k_slide<true, ZB, SRC_PEERS>, grid_for(k_slide<true, ZB, SRC_PEERS>, work),
+                    kThreads, 0, s, p, addk, slot, (const uint32_t *)nullptr, q0, q1, *peers);
+    if (fast && delta4)
+      return launch(k_slide<true, ZB, SRC_DELTA>, grid_for(k_slide<true, ZB, SRC_DELTA>, work),
+                    kThreads, 0, s, p, addk, slot, delta4, q0, q1, none);
+    if (fast)
+      return launch(k_slide<true, ZB, SRC_STAMPS>, grid_for(k_slide<true, ZB, SRC_STAMPS>, work),
+                    kThreads, 0, s, p, addk, slot, (const uint32_t *)nullptr, q0, q1, none);
+    if (p.est == 2)
+      return launch(k_slide<false, ZB, SRC_STAMPS, true>,
+                    grid_for(k_slide<false, ZB, SRC_STAMPS, true>, work), kThreads, 0, s, p, addk,
+                    slot, (const uint32_t *)nullptr, q0, q1, none);
+    return launch(k_slide<false, ZB, SRC_STAMPS>, grid_for(k_slide<false, ZB, SRC_STAMPS>, work),
+                  kThreads, 0, s, p, addk, slot, (const uint32_t *)nullptr, q0, q1, none);
   }
 };
 
@@ -458,16 +461,17 @@ cudaError_t launch_scan(const DevParams &p, int mode, const uint4 *pairs2, uint6
   const uint64_t work = n2 ? n2 : 1;
   switch (mode) {
     case 2:
-      k_scan<FAST, ZB, 2><<<grid_for(k_scan<FAST, ZB, 2>, work), kThreads, 0, s>>>(pairs2, n2, tail, p);
-      break;
+      return launch(k_scan<FAST, ZB, 2>, grid_for(k_scan<FAST, ZB, 2>, work), kThreads, 0, s,
+                    pairs2, n2, tail, p);
     case 4:
-      k_scan<FAST, ZB, 4><<<grid_for(k_scan<FAST, ZB, 4>, work), kThreads, 0, s>>>(pairs2, n2, tail, p);
-      break;
+      return launch(k_scan<FAST, ZB, 4>, grid_for(k_scan<FAST, ZB, 4>, work), kThreads, 0, s,
+                    pairs2, n2, tail, p);
     case 5:
-      k_scan<FAST, ZB, 5><<<grid_for(k_scan<FAST, ZB, 5>, work), kThreads, 0, s>>>(pairs2, n2, tail, p);
-      break;
+      return launch(k_scan<FAST, ZB, 5>, grid_for(k_scan<FAST, ZB, 5>, work), kThreads, 0, s,
+                    pairs2, n2, tail, p);
     default:
-      k_scan<FAST, ZB, 1><<<grid_for(k_scan<FAST, ZB, 1>, work), kThreads, 0, s>>>(pairs2, n2, tail, p);
+      return launch(k_scan<FAST, ZB, 1>, grid_for(k_scan<FAST, ZB, 1>, work), kThreads, 0, s, pairs2,
+                    n2, tail, p);
   }
   return cudaGetLastError();
 }

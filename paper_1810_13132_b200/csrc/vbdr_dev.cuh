@@ -95,6 +95,46 @@ struct WMax {
   static constexpr int value = (31 + Swar<ZB>::F - 1) / Swar<ZB>::F;
 };
 
+// Programmatic dependent launch (PDL): hot-path kernels are launched with
+// programmatic stream serialization, so a kernel's launch and block
+// scheduling overlap the drain of its predecessor on the stream.  Every such
+// kernel calls pdl_wait() before its first global-memory access, which blocks
+// until the predecessor grid has completed and its writes are visible -- the
+// same ordering as a plain launch, minus the launch gap.
+// Off by default: +1.7 % at caida but -20 % at 10G, where dependent CTAs
+// scheduled early unbalance the persistent grids (profiles/r01_pdl.txt).
+#ifndef VBDR_PDL
+#define VBDR_PDL 0
+#endif
+
+__device__ __forceinline__ void pdl_wait() {
+#if VBDR_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+__device__ __forceinline__ void pdl_trigger() {
+#if VBDR_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = VBDR_PDL;
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace vbdr_dev
 
 // Launchers implemented in the .cu files (host side, return cudaError_t).
