@@ -41,7 +41,11 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
 #ifndef VBDR_SCAN_CACHE_SLOTS
 #define VBDR_SCAN_CACHE_SLOTS 2048  // 16 KB per block
 #endif
+#ifndef VBDR_SCAN_THREADS
+#define VBDR_SCAN_THREADS 256
+#endif
 constexpr int kCacheSlots = VBDR_SCAN_CACHE_SLOTS;
+constexpr int kScanThreads = VBDR_SCAN_THREADS;
 
 struct ScanCache {
   unsigned long long e[kCacheSlots];  // (key << 32) | value; key = word index + 1 (0 = empty)
@@ -124,21 +128,21 @@ __device__ __forceinline__ void record(uint32_t aip, uint32_t bip, const DevPara
 
 // Grid-stride over pairs, two pairs per 16-byte load, UNROLL loads in flight.
 template <bool FAST, int ZB, int MODE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kScanThreads)
 k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict__ tail,
        DevParams p) {
   pdl_wait();
   constexpr int UNROLL = 4;
+  extern __shared__ unsigned long long scan_dyn_smem[];  // MODE 5 only (dynamic size)
   ScanCache *cache = nullptr;
   if constexpr (MODE == 5) {  // only this mode pays for the shared memory
-    __shared__ ScanCache cache_mem;
-    cache = &cache_mem;
-    for (int s = threadIdx.x; s < kCacheSlots; s += kThreads) cache->e[s] = 0ull;
+    cache = reinterpret_cast<ScanCache *>(scan_dyn_smem);
+    for (int s = threadIdx.x; s < kCacheSlots; s += kScanThreads) cache->e[s] = 0ull;
     __syncthreads();
   }
   const uint32_t tickbits = p.tick << 5;
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * kScanThreads;
+  uint64_t i = (uint64_t)blockIdx.x * kScanThreads + threadIdx.x;
   for (; i + (UNROLL - 1) * stride < n2; i += UNROLL * stride) {
     uint4 v[UNROLL];
 #pragma unroll
@@ -388,16 +392,18 @@ int sm_count() {
 // Persistent grid: as many blocks as can be resident (occupancy of this
 // kernel x SM count), never more than the work needs.
 template <typename K>
-uint32_t grid_for(K kernel, uint64_t work) {
+uint32_t grid_for(K kernel, uint64_t work, int threads = kThreads, size_t smem = 0) {
   static int resident = 0;  // one static per kernel instantiation
   if (resident == 0) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess ||
         per_sm <= 0)
       per_sm = 1;
     resident = per_sm * sm_count();
   }
-  const uint64_t need = (work + kThreads - 1) / kThreads;
+  const uint64_t need = (work + threads - 1) / threads;
   const uint64_t g = need < (uint64_t)resident ? need : (uint64_t)resident;
   return (uint32_t)(g ? g : 1);
 }
@@ -459,18 +465,20 @@ template <bool FAST, int ZB>
 cudaError_t launch_scan(const DevParams &p, int mode, const uint4 *pairs2, uint64_t n2,
                         const uint32_t *tail, cudaStream_t s) {
   const uint64_t work = n2 ? n2 : 1;
+  constexpr int T = kScanThreads;
+  constexpr size_t cache_bytes = sizeof(ScanCache);
   switch (mode) {
     case 2:
-      return launch(k_scan<FAST, ZB, 2>, grid_for(k_scan<FAST, ZB, 2>, work), kThreads, 0, s,
-                    pairs2, n2, tail, p);
+      return launch(k_scan<FAST, ZB, 2>, grid_for(k_scan<FAST, ZB, 2>, work, T), T, 0, s, pairs2,
+                    n2, tail, p);
     case 4:
-      return launch(k_scan<FAST, ZB, 4>, grid_for(k_scan<FAST, ZB, 4>, work), kThreads, 0, s,
-                    pairs2, n2, tail, p);
+      return launch(k_scan<FAST, ZB, 4>, grid_for(k_scan<FAST, ZB, 4>, work, T), T, 0, s, pairs2,
+                    n2, tail, p);
     case 5:
-      return launch(k_scan<FAST, ZB, 5>, grid_for(k_scan<FAST, ZB, 5>, work), kThreads, 0, s,
-                    pairs2, n2, tail, p);
+      return launch(k_scan<FAST, ZB, 5>, grid_for(k_scan<FAST, ZB, 5>, work, T, cache_bytes), T,
+                    cache_bytes, s, pairs2, n2, tail, p);
     default:
-      return launch(k_scan<FAST, ZB, 1>, grid_for(k_scan<FAST, ZB, 1>, work), kThreads, 0, s, pairs2,
+      return launch(k_scan<FAST, ZB, 1>, grid_for(k_scan<FAST, ZB, 1>, work, T), T, 0, s, pairs2,
                     n2, tail, p);
   }
   return cudaGetLastError();
