@@ -58,6 +58,11 @@ def parse():
     ap.add_argument("--estimator", default="hll", choices=["hll", "loglog", "pcsa"])
     ap.add_argument("--estimate", default="auto", choices=["auto", "gather", "plan"],
                     help="plan: shared-memory plan for the fixed host list (pools <= 2^22)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo + --same-device: exercise the N>1 control flow on one GPU "
+                         "(collectives on the CPU, no GPU-side waiting between ranks)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank uses cuda:0 (multi-rank logic test on a 1-GPU box)")
     ap.add_argument("--merge", default="sharded", choices=["stamps", "delta", "sharded", "p2p"],
                     help="N>1 slide merge (paper_1810_13132_b200.slide_merged)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -272,11 +277,18 @@ def run_vbdr(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    if args.same_device and args.dist_backend == "nccl" and world > 1:
+        raise SystemExit("--same-device needs --dist-backend gloo (NCCL ranks sharing a GPU "
+                         "would spin-wait on each other)")
+    gpu = 0 if args.same_device else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
         group = dist.group.WORLD
 
     tr = synth.CONFIGS[args.config]
@@ -326,7 +338,10 @@ def run_vbdr(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if args.dist_backend == "nccl":
+                dist.barrier(device_ids=[gpu])
+            else:
+                dist.barrier()
         torch.cuda.synchronize()
 
     E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -390,7 +405,7 @@ def run_vbdr(args):
     barrier()
 
     # ---- device-resident timed region (clocks sampled through it and the e2e region)
-    clocks = ClockSampler(local) if rank == 0 else None
+    clocks = ClockSampler(gpu) if rank == 0 else None
     if clocks:
         clocks.wait_first()
     # per-kernel breakdown: a first pass with events between the kernels

@@ -1,0 +1,47 @@
+"""Multi-rank runs of the real GPU path on ONE GPU: torchrun with the gloo
+backend (CPU collectives, no cross-rank GPU waiting), every merge of
+slide_merged, and bench.py's N>1 control flow."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _torchrun(n, *args):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", *args]
+    return subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+
+
+@pytest.mark.parametrize("mode", ["stamps", "delta", "sharded"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_slide_merged_multi_rank(mode, world):
+    r = _torchrun(world, os.path.join("tests", "dist_worker.py"), mode)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert f"parity=ok" in r.stdout
+
+
+def test_bench_two_ranks_gloo_same_device():
+    r = _torchrun(2, "bench.py", "--gpus", "2", "--steps", "5", "--warmup", "3", "--config", "tiny",
+                  "--dist-backend", "gloo", "--same-device", "--no-cpu-baseline")
+    assert r.returncode == 0, r.stderr[-4000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
+    assert "merge=sharded" in line["config"]["parallelism"]
