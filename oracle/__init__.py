@@ -102,6 +102,11 @@ def _declare(L):
         "orc_memory_bits": (C.c_uint64, [C.c_int, C.c_uint32, C.c_uint32]),
         "orc_estimate_M": (None, [C.c_uint32, C.c_uint32, C.c_uint64, u8p, u32p, C.c_uint64, f64p]),
         "orc_bdr_pcsa_R": (C.c_uint32, [u16p, C.c_uint32, C.c_uint32]),
+        "orc_lfpm_new": (C.c_void_p, []),
+        "orc_lfpm_free": (None, [C.c_void_p]),
+        "orc_lfpm_insert": (None, [C.c_void_p, C.c_uint64, C.c_uint32]),
+        "orc_lfpm_query": (C.c_uint32, [C.c_void_p, C.c_uint64, C.c_uint32]),
+        "orc_lfpm_len": (C.c_uint32, [C.c_void_p]),
         "orc_readout_pcsa": (None, [C.c_void_p, u8p]),
         "orc_loglog_alpha": (C.c_double, [C.c_uint64]),
         "orc_loglog_raw": (C.c_double, [u8p, C.c_uint64]),
@@ -192,6 +197,27 @@ def estimate_M(M: np.ndarray, hosts: np.ndarray, b: int, z: int, A0: int = 0x5EE
 
 
 ESTIMATORS = {"hll": 0, "loglog": 1, "pcsa": 2}
+
+
+class LFPM:
+    """The prior-art list of future possible maxima."""
+
+    def __init__(self):
+        self._h = lib().orc_lfpm_new()
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().orc_lfpm_free(self._h)
+            self._h = None
+
+    def insert(self, slice_: int, rank: int):
+        lib().orc_lfpm_insert(self._h, slice_, rank)
+
+    def query(self, t: int, k: int) -> int:
+        return lib().orc_lfpm_query(self._h, t, k)
+
+    def __len__(self):
+        return lib().orc_lfpm_len(self._h)
 
 
 def loglog_alpha(m: int) -> float:

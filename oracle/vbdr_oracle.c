@@ -485,6 +485,60 @@ void orc_estimate_variant(uint32_t b, uint32_t A0, uint64_t z, const uint8_t *V,
 }
 
 /* ------------------------------------------------------------------ */
+/* LFPM (list of future possible maxima), the prior-art sliding counter  */
+/* of LFPM-HLL the BDR replaces (section 2.3) */
+/* ------------------------------------------------------------------ */
+
+/* One LFPM: cells (slice, rank) with slices strictly increasing and ranks
+ * strictly decreasing from head to tail.  Insert removes dominated cells
+ * (rank <= new rank) from the tail, then appends; a query keeps
+ * cells with slice > t - k and returns the head's rank, or 0. */
+typedef struct {
+    uint32_t n, cap;
+    uint64_t *slice;
+    uint32_t *rank;
+} orc_lfpm;
+
+orc_lfpm *orc_lfpm_new(void)
+{
+    orc_lfpm *l = (orc_lfpm *)calloc(1, sizeof(orc_lfpm));
+    return l;
+}
+
+void orc_lfpm_free(orc_lfpm *l)
+{
+    if (!l) return;
+    free(l->slice); free(l->rank); free(l);
+}
+
+void orc_lfpm_insert(orc_lfpm *l, uint64_t slice, uint32_t rank)
+{
+    while (l->n > 0 && l->rank[l->n - 1] <= rank) l->n -= 1;
+    if (l->n == l->cap) {
+        l->cap = l->cap ? 2 * l->cap : 8;
+        l->slice = (uint64_t *)realloc(l->slice, l->cap * sizeof(uint64_t));
+        l->rank = (uint32_t *)realloc(l->rank, l->cap * sizeof(uint32_t));
+    }
+    l->slice[l->n] = slice;
+    l->rank[l->n] = rank;
+    l->n += 1;
+}
+
+uint32_t orc_lfpm_query(orc_lfpm *l, uint64_t t, uint32_t k)
+{
+    uint32_t drop = 0;
+    while (drop < l->n && l->slice[drop] + k <= t) drop += 1;  /* slice <= t - k: expired */
+    if (drop) {
+        memmove(l->slice, l->slice + drop, (l->n - drop) * sizeof(uint64_t));
+        memmove(l->rank, l->rank + drop, (l->n - drop) * sizeof(uint32_t));
+        l->n -= drop;
+    }
+    return l->n ? l->rank[0] : 0;
+}
+
+uint32_t orc_lfpm_len(const orc_lfpm *l) { return l->n; }
+
+/* ------------------------------------------------------------------ */
 /* Independent references                                               */
 /* ------------------------------------------------------------------ */
 

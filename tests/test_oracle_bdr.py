@@ -139,3 +139,55 @@ def test_table1_memory_bits():
                        (8, 60, (149, 168, 144))):
         got = tuple(oracle.memory_bits(v, b, k) for v in ("serial", "gfast", "gsmall"))
         assert got == want
+
+
+def test_lfpm_spec_vectors():
+    # SPEC.md:393-401
+    l = oracle.LFPM()
+    l.insert(0, 3)
+    l.insert(0, 5)
+    assert len(l) == 1 and l.query(0, 4) == 5          # dominated cell removed
+    l2 = oracle.LFPM()
+    l2.insert(0, 5)
+    l2.insert(0, 3)
+    assert len(l2) == 2
+    assert oracle.LFPM().query(10, 4) == 0              # empty list
+    l3 = oracle.LFPM()
+    l3.insert(2, 7)
+    assert l3.query(4, 4) == 7 and l3.query(6, 4) == 0  # inside, then expired
+
+
+@pytest.mark.parametrize("k", [1, 3, 8, 60])
+def test_bdr_equals_lfpm_windowed_max(k):
+    """SPEC.md:412, acceptance 2: the BDR (Alg.1 + Alg.2) and the
+    prior-art LFPM give the same windowed maximum at every boundary, for random
+    rank streams -- the paper's claim that BDR replaces LFPM."""
+    rng = np.random.default_rng(100 + k)
+    zb = max(1, int(np.ceil(np.log2(k + 1))))
+    for L in (5, 24):
+        for trial in range(10):
+            d = np.full(L, (1 << zb) - 1)
+            l = oracle.LFPM()
+            for t in range(4 * k + 30):
+                ranks = rng.integers(1, L + 1, size=int(rng.integers(0, 5))).tolist()
+                for r in ranks:
+                    l.insert(t, r)
+                d = oracle.bdr_end_slice_serial(d, zb, max(ranks) if ranks else 0)
+                assert oracle.bdr_GetLBP1(d, k) == l.query(t, k)
+
+
+def test_lfpm_length_is_logarithmic():
+    """SPEC.md:395 / acceptance 9: with i.i.d. geometric ranks the LFPM holds
+    about ln(n) cells after n inserts (within a factor of 2), against the BDR's
+    fixed L * zb bits (PAPER.md:76 vs Table 1)."""
+    rng = np.random.default_rng(9)
+    for n in (100, 1000, 10000):
+        lens = []
+        for _ in range(30):
+            l = oracle.LFPM()
+            # a fresh slice per insert (worst case for LFPM); rank ~ Geometric(1/2)
+            ranks = np.minimum(rng.geometric(0.5, size=n), 24)
+            for i, r in enumerate(ranks):
+                l.insert(i, int(r))
+            lens.append(len(l))
+        assert 0.5 * np.log(n) <= np.mean(lens) <= 2 * np.log(n), (n, np.mean(lens))
