@@ -57,7 +57,8 @@ typedef enum {
 
 typedef struct {
     /* m: virtual BDRs per host -- the paper's g = 2^b.  Power of
-     * two, 2 <= m, 2*m <= n_phys (R#15), n_phys / m <= 2^21 (exact sums). */
+     * two, 2 <= m, 2*m <= n_phys (R#15), n_phys * 2^L <= 2^53 (exact sums;
+     * with the default L = 32 - log2(m): n_phys / m <= 2^21). */
     uint32_t m;
     /* k: window length in slices, W(t,k).  1 <= k. */
     uint32_t k;
@@ -126,6 +127,10 @@ typedef struct {
 
 /* SYNC.  Bytes of device memory the caller must provide for this config. */
 vbdr_status vbdr_state_bytes(const vbdr_config *cfg, uint64_t *bytes);
+
+/* SYNC, host only.  NULL if cfg is valid, else why not (thread-local text,
+ * valid until the next call on this thread). */
+const char *vbdr_config_check(const vbdr_config *cfg);
 
 /* Validate cfg, bind the caller's state buffer (d_state, >= state_bytes,
  * 256-byte aligned) and initialise it on `stream`: every DR to InitDR = 2^z-1

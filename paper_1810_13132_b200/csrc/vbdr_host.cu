@@ -1,7 +1,8 @@
 // vbdr_host.cu -- the C ABI of libvbdr.so (declared in include/vbdr.h):
 // configuration validation, state-layout planning, launches, host-buffer
-// pipelines and parity exports.  No compute happens on the host: every step of
-// the path runs in the kernels of k_scan_slide.cu and k_estimate.cu.
+// pipelines, estimate plans and parity exports.  No compute happens on the
+// host: every step of the path runs in the kernels of k_scan_slide.cu,
+// k_estimate.cu and k_plan.cu.
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -67,14 +68,14 @@ double alpha_of(uint64_t s) {
   return 0.7213 / (1.0 + 1.079 / (double)s);
 }
 
-struct Plan {
+struct StateLayout {
   uint32_t b, L, zb, F, W;
   uint64_t off_acc, off_sr, off_drv, off_regmax, bytes;
 };
 
 // Validate a config and lay out the state buffer.  Returns an error text or
 // empty on success.
-std::string plan(const vbdr_config *c, vbdr_config *norm, Plan *pl) {
+std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *pl) {
   if (!c) return "null config";
   vbdr_config n = *c;
   if (n.seed_a0 == 0 && n.seed_a1 == 0) {  // R#7 defaults
@@ -94,11 +95,12 @@ std::string plan(const vbdr_config *c, vbdr_config *norm, Plan *pl) {
   if (n.n_phys < 4 || !is_pow2(n.n_phys) || n.n_phys > (1ull << 32))
     return "n_phys must be a power of two in [4, 2^32]";
   if (2ull * n.m > n.n_phys) return "2*m must be <= n_phys (vHLL denominator, R#15)";
-  if (n.n_phys / n.m > (1ull << 21)) return "n_phys/m must be <= 2^21 (exact fp64 pool sums)";
   const uint32_t b = log2u(n.m);
   if (b > 31) return "m too large";
   const uint32_t L = n.rank_cap ? n.rank_cap : 32u - b;
   if (L < 1 || L > 32u - b) return "rank_cap must be in [1, 32 - log2(m)]";
+  // the pool sum S_tot <= n_phys 2^L must convert to fp64 exactly
+  if (log2u(n.n_phys) + L > 53) return "n_phys * 2^L must be <= 2^53 (exact fp64 pool sums)";
   uint32_t zb = n.zbits;
   const bool packed = n.layout == VBDR_LAYOUT_PACKED;
   if (zb == 0) {
@@ -318,10 +320,18 @@ const char *vbdr_last_error(const vbdr_t *h) { return h ? h->err.c_str() : "null
 vbdr_status vbdr_state_bytes(const vbdr_config *cfg, uint64_t *bytes) {
   if (!bytes) return VBDR_EINVAL;
   vbdr_config n;
-  Plan pl;
-  if (!plan(cfg, &n, &pl).empty()) return VBDR_EINVAL;
+  StateLayout pl;
+  if (!layout_state(cfg, &n, &pl).empty()) return VBDR_EINVAL;
   *bytes = pl.bytes;
   return VBDR_OK;
+}
+
+const char *vbdr_config_check(const vbdr_config *cfg) {
+  static thread_local std::string msg;
+  vbdr_config n;
+  StateLayout pl;
+  msg = layout_state(cfg, &n, &pl);
+  return msg.empty() ? nullptr : msg.c_str();
 }
 
 vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, void *stream,
@@ -330,8 +340,8 @@ vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, v
   *out = nullptr;
   vbdr *h = new (std::nothrow) vbdr();
   if (!h) return VBDR_ENOMEM;
-  Plan pl;
-  std::string e = plan(cfg, &h->cfg, &pl);
+  StateLayout pl;
+  std::string e = layout_state(cfg, &h->cfg, &pl);
   if (!e.empty() || !d_state || (reinterpret_cast<uintptr_t>(d_state) & 255u)) {
     delete h;
     return VBDR_EINVAL;

@@ -48,7 +48,7 @@ SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice",
            "vbdr_export_pool_sums", "vbdr_stamp_delta", "vbdr_slide_delta", "vbdr_debug_set_tick",
            "vbdr_slide_peers", "vbdr_plan_bytes", "vbdr_plan_build", "vbdr_estimate_plan",
            "vbdr_host_sums_plan", "vbdr_plan_check", "vbdr_plan_release",
-           "vbdr_estimate_plan_host",
+           "vbdr_estimate_plan_host", "vbdr_config_check",
            "vbdr_last_error", "vbdr_status_string")
 
 _lib = None
@@ -96,6 +96,8 @@ def lib():
             f.restype = C.c_int
         L.vbdr_last_error.argtypes = [vp]
         L.vbdr_last_error.restype = C.c_char_p
+        L.vbdr_config_check.argtypes = [C.POINTER(vbdr_config)]
+        L.vbdr_config_check.restype = C.c_char_p
         L.vbdr_status_string.argtypes = [C.c_int]
         L.vbdr_status_string.restype = C.c_char_p
         _lib = L
@@ -117,7 +119,8 @@ def state_bytes(cfg: vbdr_config) -> int:
     out = C.c_uint64()
     rc = lib().vbdr_state_bytes(C.byref(cfg), C.byref(out))
     if rc != 0:
-        raise ValueError(f"vbdr_state_bytes: invalid config ({STATUS.get(rc, rc)})")
+        why = lib().vbdr_config_check(C.byref(cfg))
+        raise ValueError(f"invalid VBDR config: {why.decode() if why else STATUS.get(rc, rc)}")
     return out.value
 
 

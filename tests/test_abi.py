@@ -26,7 +26,7 @@ def test_header_declares_the_boundary():
     names = _declared()
     for n in ("vbdr_create", "vbdr_scan_slice", "vbdr_slide", "vbdr_estimate", "vbdr_destroy"):
         assert n in names
-    assert len(names) == 27
+    assert len(names) == 28
 
 
 def test_library_exports_every_declared_symbol(vb):
@@ -61,8 +61,10 @@ def test_state_bytes_and_validation(vb):
            dict(m=32, k=8, n_phys=1 << 12, zbits=3), dict(m=32, k=4, n_phys=1 << 12, rank_cap=28),
            dict(m=2, k=4, n_phys=1 << 30)]
     for kw in bad:
-        with pytest.raises(ValueError):
+        with pytest.raises(ValueError, match="invalid VBDR config: "):
             vb.state_bytes(vb.make_config(**kw))
+    # a rank cap relaxes the exact-sum bound n_phys * 2^L <= 2^53
+    vb.state_bytes(vb.make_config(2, 4, 1 << 30, rank_cap=20))
     # packed layout auto-bumps zb when k = 2^zb - 1 (R#2); explicit zb=3, k=7 is rejected
     vb.state_bytes(vb.make_config(32, 7, 1 << 12, layout="packed"))
     with pytest.raises(ValueError):
