@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--layout", default="fast", choices=["fast", "packed"])
     ap.add_argument("--scan-mode", type=int, default=0)
     ap.add_argument("--est-lanes", type=int, default=0)
+    ap.add_argument("--est-pass-log2", type=int, default=0)
     ap.add_argument("--estimator", default="hll", choices=["hll", "loglog", "pcsa"])
     ap.add_argument("--estimate", default="auto", choices=["auto", "gather", "plan"],
                     help="plan: shared-memory plan for the fixed host list (pools <= 2^22)")
@@ -299,7 +300,8 @@ def run_vbdr(args):
     if world > 1 and args.merge == "p2p":  # pool state in symmetric memory (peer-writable)
         state = PeerMerge.alloc_state(make_config(wl["m"], wl["k"], wl["n_phys"]), dev)
     pool = VBDR(wl["m"], wl["k"], wl["n_phys"], layout=args.layout, scan_mode=args.scan_mode,
-                est_lanes=args.est_lanes, estimator=args.estimator, device=dev, state=state)
+                est_lanes=args.est_lanes, est_pass_log2=args.est_pass_log2,
+                estimator=args.estimator, device=dev, state=state)
     peer = PeerMerge(pool, group) if state is not None else None
     info = pool.info()
     p0, p1 = shard_range(tr.pairs_per_slice, rank, world)
