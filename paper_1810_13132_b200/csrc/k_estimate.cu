@@ -200,13 +200,16 @@ cudaError_t run_g(const EstParams &e, const uint32_t *hosts, uint64_t n, double 
 
 namespace vbdr_launch {
 
-// Lanes per host: `lanes` if given (a power of two <= min(g, 32)), else 8
-// (best on the caida sweep, profiles/r01_sweep_caida.jsonl), capped at g.
+// Lanes per host: `lanes` if given (a power of two <= min(g, 32)), else 8 for
+// one pass (best on the caida sweep, profiles/r01_sweep_caida.jsonl) and 4 for
+// multi-pass pools (bigwin: 20.8 vs 22.4 ms, profiles/r01_pass_sweep.txt),
+// capped at g.
 cudaError_t estimate(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
                      unsigned long long *outS, uint32_t *outV, cudaStream_t s, uint32_t *nl) {
   *nl = 0;
   if (n == 0) return cudaSuccess;
-  uint32_t G = e.lanes ? e.lanes : 8u;
+  const uint32_t log2z = 31u - (uint32_t)__builtin_clz(e.mask) + 1u;
+  uint32_t G = e.lanes ? e.lanes : (e.pass_log2 < log2z ? 4u : 8u);
   if (G > e.g) G = e.g;
   if (G > 32) G = 32;
   switch (G) {
