@@ -208,6 +208,13 @@ vbdr_status vbdr_estimate(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
 vbdr_status vbdr_host_sums(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
                            uint64_t *d_S, uint32_t *d_V, void *stream);
 
+/* Super-spreader readout (the paper's motivation, PAPER.md:28,
+ * 68): write into d_idx (u32[n]) the positions j of the estimates d_est[j]
+ * >= threshold and their number into *d_count (u64, device).  The order of the
+ * positions is unspecified (sort them by estimate as needed). */
+vbdr_status vbdr_select_above(vbdr_t *h, const double *d_est, uint64_t n, double threshold,
+                              uint32_t *d_idx, uint64_t *d_count, void *stream);
+
 /* ---- plan-based estimation (a fixed host list, pools up to 2^22 BDRs) -- */
 
 /* The gather estimate reads each register with its own L2 sector request.  A

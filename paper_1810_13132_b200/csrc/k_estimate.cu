@@ -196,9 +196,39 @@ cudaError_t run_g(const EstParams &e, const uint32_t *hosts, uint64_t n, double 
   return run<G, 1, true>(e, hosts, n, out, outS, outV, s, nl);
 }
 
+// Super-spreader readout: indices of the hosts whose estimate reaches the
+// threshold, compacted with one warp-aggregated atomic per warp (order of the
+// output is unspecified; the binding sorts it).
+__global__ void __launch_bounds__(kThreads)
+k_select_above(const double *__restrict__ est, uint64_t n, double threshold,
+               uint32_t *__restrict__ idx, unsigned long long *__restrict__ count) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t n_round = (n + 31) & ~uint64_t(31);  // whole warps stay in the loop
+  for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n_round; i += stride) {
+    const bool hit = i < n && est[i] >= threshold;
+    const uint32_t ballot = __ballot_sync(0xffffffffu, hit);
+    if (ballot == 0u) continue;
+    const uint32_t lane = threadIdx.x & 31u;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(ballot));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (hit) idx[base + __popc(ballot & ((1u << lane) - 1u))] = (uint32_t)i;
+  }
+}
+
 }  // namespace
 
 namespace vbdr_launch {
+
+cudaError_t select_above(const double *est, uint64_t n, double threshold, uint32_t *idx,
+                         unsigned long long *count, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess || n == 0) return e;
+  const uint64_t need = (n + kThreads - 1) / kThreads;
+  const uint32_t grid = (uint32_t)(need < (uint64_t)sm_count() * 8 ? need : (uint64_t)sm_count() * 8);
+  k_select_above<<<grid, kThreads, 0, s>>>(est, n, threshold, idx, count);
+  return cudaGetLastError();
+}
 
 // Lanes per host: `lanes` if given (a power of two <= min(g, 32)), else 8 for
 // one pass (best on the caida sweep, profiles/r01_sweep_caida.jsonl) and 4 for

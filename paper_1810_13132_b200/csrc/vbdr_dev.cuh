@@ -199,6 +199,9 @@ cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, 
 cudaError_t estimate_plan(const EstParams &e, const PlanLayout &pl, uint64_t n, double *out,
                           unsigned long long *outS, uint32_t *outV, cudaStream_t s);
 
+cudaError_t select_above(const double *est, uint64_t n, double threshold, uint32_t *idx,
+                         unsigned long long *count, cudaStream_t s);
+
 // *nl receives the number of kernels launched (passes).
 cudaError_t estimate(const EstParams &e, const uint32_t *hosts, uint64_t n, double *out,
                      unsigned long long *outS, uint32_t *outV, cudaStream_t s, uint32_t *nl);

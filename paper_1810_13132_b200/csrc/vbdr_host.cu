@@ -504,6 +504,18 @@ vbdr_status vbdr_slide_peers(vbdr_t *h, const uint8_t *const *h_peer_delta, uint
   return after_slide(h, stream);
 }
 
+vbdr_status vbdr_select_above(vbdr_t *h, const double *d_est, uint64_t n, double threshold,
+                              uint32_t *d_idx, uint64_t *d_count, void *stream) {
+  if (!h || (n && (!d_est || !d_idx)) || !d_count) return VBDR_EINVAL;
+  if (n > 0xFFFFFFFFull) return fail(h, VBDR_ERANGE, "at most 2^32 - 1 hosts");
+  if (vbdr_status s = check_async(h, "before select_above")) return s;
+  const cudaError_t e = vbdr_launch::select_above(
+      d_est, n, threshold, d_idx, reinterpret_cast<unsigned long long *>(d_count), S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "select_above");
+  h->info.launches += n ? 1 : 0;
+  return VBDR_OK;
+}
+
 vbdr_status vbdr_plan_bytes(const vbdr_t *h, uint64_t n_hosts, uint64_t *bytes) {
   if (!h || !bytes) return VBDR_EINVAL;
   PlanGeom g;

@@ -48,7 +48,7 @@ SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice",
            "vbdr_export_pool_sums", "vbdr_stamp_delta", "vbdr_slide_delta", "vbdr_debug_set_tick",
            "vbdr_slide_peers", "vbdr_plan_bytes", "vbdr_plan_build", "vbdr_estimate_plan",
            "vbdr_host_sums_plan", "vbdr_plan_check", "vbdr_plan_release",
-           "vbdr_estimate_plan_host", "vbdr_config_check",
+           "vbdr_estimate_plan_host", "vbdr_config_check", "vbdr_select_above",
            "vbdr_last_error", "vbdr_status_string")
 
 _lib = None
@@ -83,6 +83,7 @@ def lib():
             "vbdr_estimate_plan": [vp, vp, vp, vp],
             "vbdr_host_sums_plan": [vp, vp, vp, vp, vp],
             "vbdr_estimate_plan_host": [vp, vp, vp, vp, vp],
+            "vbdr_select_above": [vp, vp, u64, C.c_double, vp, vp, vp],
             "vbdr_plan_check": [vp, vp, vp],
             "vbdr_plan_release": [vp, vp],
             "vbdr_slide_delta": [vp, vp, u64, u64, vp],
@@ -268,6 +269,30 @@ class VBDR:
                                         C.c_void_p(out.data_ptr()), _stream_ptr(stream)),
                     "vbdr_estimate")
         return out
+
+    def query_top(self, hosts, threshold: float, plan: "EstimatePlan" = None, stream=None):
+        """Hosts whose estimate reaches ``threshold``, sorted by estimate
+        (descending), ties by ascending host id: the
+        estimate (``vbdr_estimate`` or ``vbdr_estimate_plan``) and the
+        selection (``vbdr_select_above``) run on the GPU; the short selected
+        list is sorted with torch.  Returns (aip uint32 numpy, estimate float64
+        numpy)."""
+        import numpy as np
+        import torch
+        est = self.estimate_plan(plan, stream=stream) if plan is not None else \
+            self.estimate(hosts, stream=stream)
+        n = est.numel()
+        idx = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._check(lib().vbdr_select_above(self._h, C.c_void_p(est.data_ptr()), n, float(threshold),
+                                            C.c_void_p(idx.data_ptr()), C.c_void_p(cnt.data_ptr()),
+                                            _stream_ptr(stream)), "vbdr_select_above")
+        k = int(cnt.item())
+        sel = idx[:k].long()
+        e = est[sel].cpu().numpy()
+        a = hosts[sel].cpu().numpy().view(np.uint32)
+        order = np.lexsort((a, -e))
+        return a[order], e[order]
 
     # ---------------------------------------------------- plan-based estimate
     def plan(self, hosts, stream=None):

@@ -602,3 +602,31 @@ def test_plan_refuses_large_pools():
     pool = VBDR(256, 10, 1 << 23, device=DEV)
     with pytest.raises(ValueError):
         pool.plan(dev_u32(np.arange(10, dtype=np.uint32)))
+
+
+def test_query_top_super_spreaders():
+    """hosts at or above a threshold, sorted by estimate
+    (descending), ties by ascending aip -- against the oracle's estimates."""
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial")
+    pool = VBDR(32, 4, 1 << 12, device=DEV)
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    for t in range(6):
+        pairs = synth.generate(tr, t)
+        pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+    want = ref.estimate(ref.readout(), hosts_np)
+    for thr in (0.0, 100.0, 500.0, 1e9):
+        aips, ests = pool.query_top(hosts, thr)
+        sel = want >= thr
+        exp_a = hosts_np[sel]
+        order = np.lexsort((exp_a, -want[sel]))
+        assert np.array_equal(aips, exp_a[order]), thr
+        assert np.allclose(ests, want[sel][order], rtol=1e-9)
+    plan = pool.plan(hosts)
+    a2, e2 = pool.query_top(hosts, 100.0, plan=plan)
+    a1, e1 = pool.query_top(hosts, 100.0)
+    assert np.array_equal(a1, a2) and np.array_equal(e1, e2)
