@@ -67,6 +67,10 @@ def parse():
     ap.add_argument("--merge", default="sharded", choices=["stamps", "delta", "sharded", "p2p"],
                     help="N>1 slide merge (paper_1810_13132_b200.slide_merged)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="headline from pipelined steps: the estimate of slice t overlaps the "
+                         "scan of slice t+1 on a second stream (profiles/r01_pipeline.txt: "
+                         "+3 %% at caida, -20 %% at 10G with scan mode 5; default off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--flush-mib", type=int, default=512)
@@ -329,11 +333,11 @@ def run_vbdr(args):
                 raise
             plan = None
 
-    def estimate(out):
+    def estimate(out, on=None):
         if plan is not None:
-            pool.estimate_plan(plan, out=out)
+            pool.estimate_plan(plan, out=out, stream=on)
         else:
-            pool.estimate(hosts, out=out)
+            pool.estimate(hosts, out=out, stream=on)
     flush = torch.empty(args.flush_mib << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     torch.cuda.synchronize()
@@ -400,6 +404,24 @@ def run_vbdr(args):
         estimate(est_out)
         mark(evs, 5)
 
+    stream_b = torch.cuda.Stream(dev)
+    ev_closed, ev_est = torch.cuda.Event(), torch.cuda.Event()
+
+    def step_pipelined(i):
+        """Steady-state software pipeline: the estimate of the slice closed
+        last (t) runs on a second stream while the scan of slice t+1 runs on
+        the main one; the slide of t+1 then waits for that estimate (it
+        rewrites the registers the estimate reads).  Same work per step as
+        step(): one scan, one slide, one estimate."""
+        x = inputs[i % n_inputs]
+        ev_closed.record(stream)
+        stream_b.wait_event(ev_closed)
+        estimate(est_out, stream_b)
+        ev_est.record(stream_b)
+        pool.scan_slice(x)
+        stream.wait_event(ev_est)
+        close_slice()
+
     # warm-up
     for i in range(args.warmup):
         flush.fill_(i & 0xFF)
@@ -420,18 +442,25 @@ def run_vbdr(args):
     ms = np.array([[ev[j].elapsed_time(ev[j + 1]) for j in range(5)] for ev in events])
     ms_k = ms.mean(axis=0)  # scan, merge, slide, gather, estimate
     per_kernel_local = np.array([ms_k[0], ms_k[1] + ms_k[3], ms_k[2], ms_k[4]])
-    # headline: events only around each step (nothing between its kernels)
-    step_ev = [(E(), E()) for _ in range(args.steps)]
-    launches0 = pool.info()["launches"]
-    barrier()
-    for i in range(args.steps):
-        flush.fill_(i & 0xFF)  # L2 flush (> 126 MB L2), outside the step events
-        step_ev[i][0].record(stream)
-        step(args.warmup + args.steps + i)
-        step_ev[i][1].record(stream)
-    barrier()
-    launches = pool.info()["launches"] - launches0
-    local_total = float(sum(a.elapsed_time(b) for a, b in step_ev))
+    # serial steps, events only around each step (nothing between its kernels)
+    def timed_steps(fn, first):
+        evs = [(E(), E()) for _ in range(args.steps)]
+        l0 = pool.info()["launches"]
+        barrier()
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)  # L2 flush (> 126 MB L2), outside the step events
+            evs[i][0].record(stream)
+            fn(first + i)
+            evs[i][1].record(stream)
+        barrier()
+        return float(sum(a.elapsed_time(b) for a, b in evs)), pool.info()["launches"] - l0
+
+    serial_total, serial_launches = timed_steps(step, args.warmup + args.steps)
+    # headline: the pipelined steady state (same work per step)
+    if args.pipeline:
+        local_total, launches = timed_steps(step_pipelined, args.warmup + 2 * args.steps)
+    else:
+        local_total, launches = serial_total, serial_launches
     if world > 1:
         t = torch.tensor([local_total, *per_kernel_local.tolist()], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -441,6 +470,11 @@ def run_vbdr(args):
         total_ms = local_total
         per_kernel = per_kernel_local
     ms_per_step = total_ms / args.steps
+    serial_ms = serial_total / args.steps
+    if world > 1:
+        t = torch.tensor([serial_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        serial_ms = float(t[0])
     value = tr.pairs_per_slice / (ms_per_step * 1e-3) / 1e6
 
     # ---- end to end through the host-buffer C ABI entry points
@@ -552,13 +586,16 @@ def run_vbdr(args):
     line = {
         "metric": "IP pairs scanned per second through whole slices (scan + slide + estimate)",
         "value": round(value, 3), "unit": "Mpairs/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+        "ms_per_step_serial": round(serial_ms, 5), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": args.config, "layout": args.layout, **wl,
                    "pairs_per_slice": tr.pairs_per_slice, "hosts": tr.hosts,
                    "parallelism": (f"pairs+hosts sharded x{world}, merge={args.merge}"
                                    if world > 1 else "single GPU"),
                    "l2": f"flushed before every step ({args.flush_mib} MiB write)",
+                   "schedule": ("pipelined: estimate(t) on a 2nd stream overlaps scan(t+1)"
+                                if args.pipeline else "serial"),
                    "scan_mode": args.scan_mode, "est_lanes": args.est_lanes,
                    "estimator": args.estimator,
                    "estimate_path": "plan" if plan is not None else "gather",
