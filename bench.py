@@ -562,11 +562,11 @@ def run_vbdr(args):
     }
     if plan is not None:
         # The plan path streams, per slice: 4 B of plan entry per gather, the
-        # run starts, the register array once per SM (from L2; counted once
+        # round starts, the register array once per SM (from L2; counted once
         # here as DRAM bytes), 8 B of estimate per host.
         ctas = torch.cuda.get_device_properties(dev).multi_processor_count
         phases = max(1, wl["n_phys"] >> 16)
-        plan_bytes = 4 * gathers + 4 * ctas * phases * 516 + wl["n_phys"] + 8 * (h1 - h0)
+        plan_bytes = 4 * gathers + 4 * ctas * phases * 20 + wl["n_phys"] + 8 * (h1 - h0)
         plan_gbs = plan_bytes / (kern["estimate"] * 1e-3) / 1e9
         kernels["estimate"] = {
             "ms": kern["estimate"], "path": "plan", "bound": "hbm", "achieved": round(plan_gbs, 1),

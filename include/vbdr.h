@@ -219,12 +219,13 @@ vbdr_status vbdr_select_above(vbdr_t *h, const double *d_est, uint64_t n, double
 
 /* The gather estimate reads each register with its own L2 sector request.  A
  * PLAN preprocesses a host list once: every (host, i) gather of Alg.5 is
- * precomputed and grouped by 64 KB block of the register array; per slice the
- * estimate then streams the array block by block through shared memory (TMA
- * bulk copies) and every thread adds its hosts' registers from there.  Same
- * integer sums, same fp64 finish: results are bit-identical to
- * vbdr_estimate.  Needs n_phys in [64, 2^22] and n_hosts <= 7 * 512 * SMs
- * (530k on B200); otherwise VBDR_ERANGE. */
+ * precomputed and grouped by 64 KB block of the register array and by warp,
+ * as rounds of 32 entries; per slice the estimate then streams the array block
+ * by block through shared memory (TMA bulk copies) and every lane adds one
+ * register per round into its host's shared-memory accumulator.  Same integer
+ * sums, same fp64 finish: results are bit-identical to vbdr_estimate.  Needs
+ * n_phys in [64, 2^22], n_hosts <= 7 * 512 * SMs (530k on B200) and
+ * g * 2^(L-1) (HLL) or g * 255 below 2^32; otherwise VBDR_ERANGE. */
 
 /* SYNC, host only.  Bytes of the caller's plan buffer for n_hosts hosts. */
 vbdr_status vbdr_plan_bytes(const vbdr_t *h, uint64_t n_hosts, uint64_t *bytes);

@@ -5,17 +5,25 @@
 // rate: one 32-byte sector request per 1-byte register read.  For pools whose
 // register array is small (n_phys <= 2^22, 4 MiB) the same sums can be formed
 // from shared memory instead:
-//   * a PLAN, built once per host list, assigns every host to one thread of
-//     one of `ctas` persistent CTAs (host h -> thread h % T, slot h / T) and
-//     lists, for every (CTA, register block of 2^16) phase, the entries
-//     (offset in block | slot << 16) of each thread's (host, i) gathers that
-//     fall in that block (Alg.5 / Alg.3 indices, precomputed);
+//   * a PLAN, built once per host list, assigns every host to an accumulator
+//     slot of one warp of one of `ctas` persistent CTAs, spreading hosts over
+//     CTAs first, then warps, then lanes (host_slot below), and lists, for
+//     every (CTA, register block of 2^16)
+//     phase and every warp, the warp's (host, i) gathers that fall in that
+//     block (Alg.5 / Alg.3 indices, precomputed) as ROUNDS of 32 entries
+//     (offset in block | accumulator index << 16), one entry per lane.  Any
+//     lane may serve any of its warp's hosts, so all lanes stay busy (a
+//     thread-owns-its-hosts layout idles ~35 % of the lanes on the longest
+//     run); within a group the entries are ordered by shared-memory bank of
+//     their register and striped over the rounds (sorted index i -> round
+//     i mod R, lane i / R), so one round touches each bank about once;
 //   * per slice, each CTA streams the register array through shared memory
 //     one 64 KB block at a time (TMA bulk copies, double buffered, mbarrier),
-//     together with its entries for that block, and every thread adds
-//     2^(L - M) (or M for LogLog/PCSA) and the zero count into its hosts'
-//     packed accumulators (S | V << 40) in shared memory -- no atomics, no
-//     L2 gathers.  The last step is the fp64 finish of k_estimate.
+//     together with its entries for that block, and every lane adds
+//     2^(L - M) for M >= 1 (M for LogLog/PCSA) into the entry's u32
+//     accumulator with a shared-memory atomic, and counts M == 0 in a second
+//     array (S = S' + V 2^L; S' <= g 2^(L-1) = 2^31 for L = 32 - log2 g)
+//     -- no L2 gathers.  The last step is the fp64 finish of k_estimate.
 // Integer sums make the result bit-identical to the gather kernel.
 #include "vbdr_dev.cuh"
 
@@ -25,10 +33,12 @@ using vbdr_launch::PlanLayout;
 
 namespace {
 
-constexpr int kT = vbdr_launch::kPlanThreads;  // 512
-constexpr int kSlots = vbdr_launch::kPlanSlots;  // 7
-constexpr int kCap = vbdr_launch::kPlanEntCap;   // entries per (CTA, phase) buffer
-constexpr int kStride = kT + 4;                  // run starts per key, 16-byte padded
+constexpr int kT = vbdr_launch::kPlanThreads;   // 512
+constexpr int kW = kT / 32;                     // 16 warps
+constexpr int kSlots = vbdr_launch::kPlanSlots; // 7
+constexpr int kCap = vbdr_launch::kPlanEntCap;  // entries per (CTA, phase) buffer
+constexpr int kStride = vbdr_launch::kPlanStride;  // round starts per key (kW + 1 used)
+constexpr int kAccW = kSlots * 32 + 32;         // per warp: host slots + one trash word per lane
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -39,25 +49,37 @@ struct BuildArgs {
   const uint32_t *hosts;
   uint64_t n;
   uint32_t g, A0, mask, block_log2, phases, ctas;
-  uint32_t *counts;      // [ctas * phases * kT]
-  uint32_t *starts;      // [ctas * phases * kStride]
-  uint32_t *range_base;  // [ctas * phases + 1]
+  uint32_t *counts;      // [ctas * phases * kW * 32]: per (group, bank) counts, then cursors
+  uint32_t *starts;      // [ctas * phases * kStride]: round offsets of the kW warps of a key
+  uint32_t *range_base;  // [ctas * phases + 1], in entries
   uint32_t *entries;
   uint32_t *max_range;   // scalar
 };
 
+// Host h -> CTA h % ctas; q = h / ctas -> warp q % 16, lane (q / 16) % 32,
+// slot q / 512: short host lists still use every CTA and warp.
+__host__ __device__ __forceinline__ uint64_t slot_host(uint32_t cta, uint32_t warp, uint32_t lane,
+                                                       uint32_t slot, uint32_t ctas) {
+  return ((uint64_t)slot * kT + lane * kW + warp) * ctas + cta;
+}
+
+// (host, i) -> key = (CTA, phase), warp, bank of the register in the block,
+// and the entry value (offset in block | accumulator index << 16).
 __device__ __forceinline__ void locate_entry(const BuildArgs &a, uint64_t h, uint32_t i,
-                                             uint64_t &key, uint32_t &thread, uint32_t &val) {
-  const uint64_t T = (uint64_t)a.ctas * kT;
-  const uint64_t t = h % T;
-  const uint32_t slot = (uint32_t)(h / T);
-  const uint32_t cta = (uint32_t)(t / kT);
-  thread = (uint32_t)(t % kT);
-  const uint32_t s1 = fmix32(i ^ a.A0);                         // Alg.3
+                                             uint64_t &key, uint32_t &warp, uint32_t &bank,
+                                             uint32_t &val) {
+  const uint32_t cta = (uint32_t)(h % a.ctas);
+  const uint64_t q = h / a.ctas;
+  warp = (uint32_t)(q % kW);
+  const uint32_t lane = (uint32_t)((q / kW) % 32u);
+  const uint32_t slot = (uint32_t)(q / kT);
+  const uint32_t s1 = fmix32(i ^ a.A0);                            // Alg.3
   const uint32_t pidx = fmix32(__ldg(a.hosts + h) ^ s1) & a.mask;  // Alg.3
   const uint32_t phase = pidx >> a.block_log2;
+  const uint32_t off = pidx & ((1u << a.block_log2) - 1u);
   key = (uint64_t)cta * a.phases + phase;
-  val = (pidx & ((1u << a.block_log2) - 1u)) | (slot << 16);
+  bank = (off >> 2) & 31u;
+  val = off | ((slot * 32u + lane) << 16);
 }
 
 __global__ void k_plan_count(BuildArgs a) {
@@ -65,45 +87,45 @@ __global__ void k_plan_count(BuildArgs a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += stride) {
     uint64_t key;
-    uint32_t thread, val;
-    locate_entry(a, x / a.g, (uint32_t)(x % a.g), key, thread, val);
-    atomicAdd(a.counts + key * kT + thread, 1u);
+    uint32_t warp, bank, val;
+    locate_entry(a, x / a.g, (uint32_t)(x % a.g), key, warp, bank, val);
+    atomicAdd(a.counts + (key * kW + warp) * 32 + bank, 1u);
   }
 }
 
-// One block per key: exclusive scan of the kT thread counts -> run starts;
-// the key's total (padded to a multiple of 4 entries: 16-byte ranges).
+// One block per key, thread (warp w, lane b) = group w's bank b: exclusive
+// scan of the bank counts -> bank starts in the group's sorted order (the
+// fill cursors); group sizes n_w -> R_w = ceil(n_w / 32) rounds; exclusive
+// scan over the warps -> round offsets; the key's entries = 32 * sum R_w.
 __global__ void __launch_bounds__(kT) k_plan_starts(BuildArgs a, uint32_t *range_size) {
-  __shared__ uint32_t warp_sum[kT / 32];
+  __shared__ uint32_t rounds[kW];
   const uint64_t key = blockIdx.x;
-  const uint32_t c = a.counts[key * kT + threadIdx.x];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t *cnt = a.counts + key * kT + threadIdx.x;
+  const uint32_t c = *cnt;
   uint32_t x = c;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
     if (lane >= (uint32_t)off) x += y;
   }
-  if (lane == 31) warp_sum[w] = x;
+  *cnt = x - c;  // cursor: sorted index of this bank's first entry
+  if (lane == 31) rounds[w] = (x + 31u) >> 5;
   __syncthreads();
   if (w == 0) {
-    uint32_t v = lane < kT / 32 ? warp_sum[lane] : 0u;
+    const uint32_t r = lane < kW ? rounds[lane] : 0u;
+    uint32_t v = r;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, v, off);
       if (lane >= (uint32_t)off) v += y;
     }
-    if (lane < kT / 32) warp_sum[lane] = v;
+    if (lane <= kW) a.starts[key * kStride + lane] = v - r;  // lane kW: the key's total
+    if (lane == kW) {
+      range_size[key] = 32u * (v - r);
+      atomicMax(a.max_range, 32u * (v - r));
+    }
   }
-  __syncthreads();
-  const uint32_t incl = x + (w > 0 ? warp_sum[w - 1] : 0u);
-  a.starts[key * kStride + threadIdx.x] = incl - c;
-  if (threadIdx.x == kT - 1) {
-    a.starts[key * kStride + kT] = incl;
-    range_size[key] = (incl + 3u) & ~3u;
-    atomicMax(a.max_range, incl);
-  }
-  a.counts[key * kT + threadIdx.x] = 0u;  // reused as fill cursors
 }
 
 // Single block: exclusive scan of the range sizes -> range_base (u32 entries).
@@ -144,15 +166,34 @@ __global__ void __launch_bounds__(1024) k_plan_bases(BuildArgs a, const uint32_t
   if (threadIdx.x == 0) a.range_base[nkeys] = carry;
 }
 
+// Entry with sorted index i of a group of R rounds -> round i % R, lane i / R.
+__device__ __forceinline__ uint32_t stripe(uint32_t i, uint32_t R) {
+  return (i % R) * 32u + i / R;
+}
+
 __global__ void k_plan_fill(BuildArgs a) {
   const uint64_t total = a.n * a.g;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += stride) {
     uint64_t key;
-    uint32_t thread, val;
-    locate_entry(a, x / a.g, (uint32_t)(x % a.g), key, thread, val);
-    const uint32_t k = atomicAdd(a.counts + key * kT + thread, 1u);
-    a.entries[a.range_base[key] + a.starts[key * kStride + thread] + k] = val;
+    uint32_t warp, bank, val;
+    locate_entry(a, x / a.g, (uint32_t)(x % a.g), key, warp, bank, val);
+    const uint32_t i = atomicAdd(a.counts + (key * kW + warp) * 32 + bank, 1u);
+    const uint32_t r0 = a.starts[key * kStride + warp], R = a.starts[key * kStride + warp + 1] - r0;
+    a.entries[a.range_base[key] + 32u * r0 + stripe(i, R)] = val;
+  }
+}
+
+// One block per key, warp w pads group w: sorted indices [n_w, 32 R_w) get
+// the lane's trash accumulator (offset 0 is a valid register to read).
+__global__ void __launch_bounds__(kT) k_plan_pad(BuildArgs a) {
+  const uint64_t key = blockIdx.x;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t n_w = a.counts[(key * kW + w) * 32 + 31];  // cursor of the last bank = n_w
+  const uint32_t r0 = a.starts[key * kStride + w], R = a.starts[key * kStride + w + 1] - r0;
+  for (uint32_t i = n_w + lane; i < 32u * R; i += 32u) {
+    const uint32_t pos = stripe(i, R);
+    a.entries[a.range_base[key] + 32u * r0 + pos] = (uint32_t)(kSlots * 32 + (pos & 31u)) << 16;
   }
 }
 
@@ -169,7 +210,8 @@ struct __align__(128) PlanSmem {
   uint8_t tab[2][1 << BLOCK_LOG2];
   uint32_t ent[2][kCap];
   uint32_t start[2][kStride];
-  unsigned long long acc[kSlots][kT];
+  uint32_t acc[kW][kAccW];   // S' = sum over M >= 1 of 2^(L - M) (HLL) or M
+  uint32_t accv[kW][kAccW];  // V = number of M == 0
   uint64_t bar[2];
   double etot_z;
 };
@@ -183,9 +225,11 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
   pdl_wait();
   extern __shared__ __align__(128) uint8_t raw[];
   PlanSmem<BLOCK_LOG2> &sm = *reinterpret_cast<PlanSmem<BLOCK_LOG2> *>(raw);
-  const int tid = threadIdx.x;
-#pragma unroll
-  for (int s = 0; s < kSlots; ++s) sm.acc[s][tid] = 0ull;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int i = lane; i < kAccW; i += 32) {
+    sm.acc[w][i] = 0u;
+    sm.accv[w][i] = 0u;
+  }
   if (tid == 0) {
     for (int b = 0; b < 2; ++b)
       asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[b])));
@@ -214,7 +258,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
     const int b = ph & 1;
     const uint64_t key = (uint64_t)blockIdx.x * phases + ph;
     const uint32_t e0 = pl.range_base[key], e1 = pl.range_base[key + 1];
-    const uint32_t ebytes = (e1 - e0) * 4u;  // ranges are multiples of 4 entries
+    const uint32_t ebytes = (e1 - e0) * 4u;  // ranges are multiples of 32 entries
     const uint32_t sbytes = kStride * 4u;
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.bar[b])),
                  "r"(BLOCK + ebytes + sbytes)
@@ -224,6 +268,8 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
     bulk(sm.start[b], pl.starts + key * kStride, sbytes, &sm.bar[b]);
   };
   if (tid == 0) issue(0);
+  uint32_t *acc = sm.acc[w];
+  uint32_t *accv = sm.accv[w];
   for (uint32_t ph = 0; ph < phases; ++ph) {
     const int b = ph & 1;
     if (tid == 0 && ph + 1 < phases) issue(ph + 1);  // buffer freed by the sync of phase ph-1
@@ -241,27 +287,27 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
       }
     }
     const uint8_t *tab = sm.tab[b];
-    const uint32_t k0 = sm.start[b][tid], k1 = sm.start[b][tid + 1];
-    for (uint32_t k = k0; k < k1; ++k) {
-      const uint32_t v = sm.ent[b][k];
+    const uint32_t r0 = sm.start[b][w], r1 = sm.start[b][w + 1];
+    const uint32_t *ent = sm.ent[b] + lane;
+#pragma unroll 4
+    for (uint32_t r = r0; r < r1; ++r) {  // one entry per lane per round
+      const uint32_t v = ent[r * 32u];
       const uint32_t M = tab[v & (BLOCK - 1u)];
-      const unsigned long long c =
-          e.est == 0u ? 1ull << (e.L - M) : (unsigned long long)M;  // HLL / LogLog, PCSA
-      sm.acc[v >> 16][tid] += c + ((unsigned long long)(M == 0u) << 40);
+      // one atomic per lane: the zero count or S' (same bank either way)
+      const uint32_t c = e.est == 0u ? 1u << (e.L - M) : M;  // HLL / LogLog, PCSA
+      atomicAdd((M == 0u ? accv : acc) + (v >> 16), M == 0u ? 1u : c);
     }
     __syncthreads();
   }
   pdl_trigger();
-  const uint64_t T = (uint64_t)gridDim.x * kT;
-  const uint64_t t = (uint64_t)blockIdx.x * kT + tid;
   const double g = (double)e.g;
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
-    const uint64_t h = (uint64_t)s * T + t;
+    const uint64_t h = slot_host(blockIdx.x, w, lane, s, gridDim.x);
     if (h >= n) break;
-    const unsigned long long packed = sm.acc[s][tid];
-    const unsigned long long S = packed & ((1ull << 40) - 1ull);
-    const uint32_t V = (uint32_t)(packed >> 40);
+    const uint32_t V = accv[s * 32 + lane];
+    const unsigned long long S =
+        acc[s * 32 + lane] + (e.est == 0u ? (unsigned long long)V << e.L : 0ull);
     if constexpr (SUMS) {
       outS[h] = S;
       outV[h] = V;
@@ -310,7 +356,7 @@ cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, 
   a.entries = pl.entries;
   a.max_range = pl.max_range;
   const uint64_t nkeys = (uint64_t)pl.ctas * pl.phases;
-  cudaError_t e = cudaMemsetAsync(pl.counts, 0, nkeys * kT * 4, s);
+  cudaError_t e = cudaMemsetAsync(pl.counts, 0, nkeys * kW * 32 * 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(pl.max_range, 0, 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(pl.error, 0, 8, s);
   if (e != cudaSuccess) return e;
@@ -320,6 +366,7 @@ cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, 
   k_plan_starts<<<(uint32_t)nkeys, kT, 0, s>>>(a, range_size_scratch);
   k_plan_bases<<<1, 1024, 0, s>>>(a, range_size_scratch, nkeys);
   k_plan_fill<<<grid ? grid : 1, 256, 0, s>>>(a);
+  k_plan_pad<<<(uint32_t)nkeys, kT, 0, s>>>(a);
   return cudaGetLastError();
 }
 

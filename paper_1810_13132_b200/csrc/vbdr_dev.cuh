@@ -179,16 +179,17 @@ struct EstParams {
   double coef_z;      // same for the pool of z registers
 };
 // Plan-based estimate (k_plan.cu): a host list preprocessed into per-(CTA,
-// register block) entry runs.  Layout of the caller's plan buffer.
+// register block, warp) rounds of 32 entries.  Layout of the caller's plan buffer.
 constexpr int kPlanThreads = 512;
-constexpr int kPlanSlots = 7;     // hosts per thread
+constexpr int kPlanSlots = 7;     // hosts per thread (accumulator slots per lane)
 constexpr int kPlanEntCap = 8192; // entries per (CTA, block) staged in shared memory
+constexpr int kPlanStride = 20;   // round starts per (CTA, block): 16 warps + total, 16-byte padded
 struct PlanLayout {
   uint32_t ctas, phases, block_log2;
   uint64_t n_hosts;
-  uint32_t *range_base;  // [ctas * phases + 1]
-  uint32_t *starts;      // [ctas * phases * (kPlanThreads + 4)]
-  uint32_t *counts;      // [ctas * phases * kPlanThreads] (build scratch)
+  uint32_t *range_base;  // [ctas * phases + 1], entries
+  uint32_t *starts;      // [ctas * phases * kPlanStride], rounds
+  uint32_t *counts;      // [ctas * phases * kPlanThreads] (build scratch: per (warp, bank))
   uint32_t *range_size;  // [ctas * phases] (build scratch)
   uint32_t *entries;
   uint32_t *max_range;   // build: largest (CTA, block) entry count

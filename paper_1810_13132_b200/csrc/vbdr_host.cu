@@ -229,6 +229,11 @@ bool plan_geom(const vbdr *h, uint64_t n_hosts, PlanGeom *g) {
   if (sms <= 0) sms = 148;
   const uint64_t T = (uint64_t)sms * vbdr_launch::kPlanThreads;
   if (n_hosts == 0 || n_hosts > T * vbdr_launch::kPlanSlots) return false;
+  // per-host S' (registers with M >= 1) accumulates in a u32 in shared memory:
+  // at most g * 2^(L-1) (HLL) or g * 255
+  const uint64_t smax =
+      (uint64_t)h->cfg.m * (h->cfg.estimator == 0 ? 1ull << (h->p.L - 1) : 255ull);
+  if (smax >> 32) return false;
   g->ctas = (uint32_t)sms;
   g->block_log2 = z >= (1ull << 16) ? 16u : (uint32_t)log2u(z);
   g->phases = (uint32_t)(z >> g->block_log2);
@@ -240,11 +245,13 @@ bool plan_geom(const vbdr *h, uint64_t n_hosts, PlanGeom *g) {
     return o;
   };
   g->off_range_base = take(4 * (g->nkeys + 1));
-  g->off_starts = take(4 * g->nkeys * (vbdr_launch::kPlanThreads + 4));
+  g->off_starts = take(4 * g->nkeys * vbdr_launch::kPlanStride);
   g->off_counts = take(4 * g->nkeys * vbdr_launch::kPlanThreads);
   g->off_range_size = take(4 * g->nkeys);
   g->off_misc = take(64);
-  g->off_entries = take(4 * (n_hosts * h->cfg.m + 4 * g->nkeys));
+  // every (CTA, block, warp) group is padded to whole rounds of 32 entries
+  const uint64_t groups = g->nkeys * (vbdr_launch::kPlanThreads / 32);
+  g->off_entries = take(4 * (n_hosts * h->cfg.m + 31 * groups));
   g->bytes = off;
   return true;
 }
@@ -543,7 +550,7 @@ vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts
     e = cudaMemcpyAsync(&max_range, pl.max_range, 4, cudaMemcpyDeviceToHost, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e != cudaSuccess) return cuda_fail(h, e, "plan_build");
-  h->info.launches += 4;
+  h->info.launches += 5;
   if (max_range > (uint32_t)vbdr_launch::kPlanEntCap) {
     h->plans.erase(d_plan);
     return fail(h, VBDR_ERANGE, "a register block holds more entries than shared memory stages");

@@ -598,6 +598,32 @@ def test_plan_estimate_caida_full_size():
     pool.plan_check(plan)
 
 
+@pytest.mark.parametrize("g,z_log2,n_hosts", [(64, 12, 1001), (16, 12, 3),
+                                               (32, 20, 7 * 512 * 148 - 5)])
+def test_plan_accumulator_modes_and_ragged_hosts(g, z_log2, n_hosts):
+    """Plan rounds for a host list with duplicates and a ragged tail, for 3
+    hosts (almost every round is padding) and for the largest host count a
+    plan takes (20 blocks of 2^16 registers): bit-identical to the gather
+    estimate and sums."""
+    tr = synth.CONFIGS["tiny"]
+    pool = VBDR(g, 4, 1 << z_log2, device=DEV)
+    rng = np.random.default_rng(g + n_hosts)
+    hosts_np = rng.integers(0, 2**32, n_hosts, dtype=np.uint64).astype(np.uint32)
+    hosts_np[1::7][:64] = hosts_np[0]  # duplicates (many would pile into a few blocks)
+    hosts = dev_u32(hosts_np)
+    plan = pool.plan(hosts)
+    for t in range(6):
+        pool.scan_slice(dev_u32(synth.generate(tr, t)))
+        pool.slide()
+        if t >= 3:
+            assert np.array_equal(pool.estimate_plan(plan).cpu().numpy(),
+                                  pool.estimate(hosts).cpu().numpy())
+            S1, V1 = pool.host_sums_plan(plan)
+            S2, V2 = pool.host_sums(hosts)
+            assert torch.equal(S1, S2) and torch.equal(V1, V2)
+    pool.plan_check(plan)
+
+
 def test_plan_refuses_large_pools():
     pool = VBDR(256, 10, 1 << 23, device=DEV)
     with pytest.raises(ValueError):
