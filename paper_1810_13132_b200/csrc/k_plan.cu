@@ -33,6 +33,10 @@ using vbdr_launch::PlanLayout;
 
 namespace {
 
+#ifndef VBDR_PLAN_SORT
+#define VBDR_PLAN_SORT 0
+#endif
+
 constexpr int kT = vbdr_launch::kPlanThreads;   // 512
 constexpr int kW = kT / 32;                     // 16 warps
 constexpr int kSlots = vbdr_launch::kPlanSlots; // 7
@@ -78,7 +82,13 @@ __device__ __forceinline__ void locate_entry(const BuildArgs &a, uint64_t h, uin
   const uint32_t phase = pidx >> a.block_log2;
   const uint32_t off = pidx & ((1u << a.block_log2) - 1u);
   key = (uint64_t)cta * a.phases + phase;
-  bank = (off >> 2) & 31u;
+#if VBDR_PLAN_SORT == 1
+  bank = lane;  // accumulator bank
+#elif VBDR_PLAN_SORT == 2
+  bank = ((off >> 2) + lane) & 31u;
+#else
+  bank = (off >> 2) & 31u;  // register bank in the staged block
+#endif
   val = off | ((slot * 32u + lane) << 16);
 }
 
@@ -212,27 +222,49 @@ struct __align__(128) PlanSmem {
   uint32_t start[2][kStride];
   uint32_t acc[kW][kAccW];   // S' = sum over M >= 1 of 2^(L - M) (HLL) or M
   uint32_t accv[kW][kAccW];  // V = number of M == 0
-  uint64_t bar[2];
+  uint64_t full[2];          // TMA bytes of buffer b landed
+  uint64_t empty[2];         // all kW consumer warps are done with buffer b
   double etot_z;
 };
 
+__device__ __forceinline__ bool mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t spin = 0; !done; ++spin) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (spin > (1u << 26)) return false;  // a lost transfer must not hang the GPU
+  }
+  return true;
+}
+
+// kW consumer warps + one producer warp (TMA issue only).  Buffers are
+// handed over with full / empty mbarriers, so a warp that finishes a block
+// early starts on the next one instead of waiting at a CTA barrier.
 template <int BLOCK_LOG2, bool SUMS>
-__global__ void __launch_bounds__(kT, 1)
+__global__ void __launch_bounds__(kT + 32, 1)
 k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out,
                 unsigned long long *__restrict__ outS, uint32_t *__restrict__ outV,
                 unsigned long long *__restrict__ err) {
   constexpr uint32_t BLOCK = 1u << BLOCK_LOG2;
+  constexpr int ILP = 4;
   pdl_wait();
   extern __shared__ __align__(128) uint8_t raw[];
   PlanSmem<BLOCK_LOG2> &sm = *reinterpret_cast<PlanSmem<BLOCK_LOG2> *>(raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int i = lane; i < kAccW; i += 32) {
-    sm.acc[w][i] = 0u;
-    sm.accv[w][i] = 0u;
+  if (w < kW) {
+    for (int i = lane; i < kAccW; i += 32) {
+      sm.acc[w][i] = 0u;
+      sm.accv[w][i] = 0u;
+    }
   }
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b)
-      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar[b])));
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&sm.full[b])));
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(&sm.empty[b])), "r"(kW));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (!SUMS) {
       const unsigned long long St = e.acc[0], Vt = e.acc[1];
@@ -247,57 +279,72 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
   }
   __syncthreads();
   const uint32_t phases = pl.phases;
-  auto bulk = [&](void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-  };
-  auto issue = [&](uint32_t ph) {
-    const int b = ph & 1;
-    const uint64_t key = (uint64_t)blockIdx.x * phases + ph;
-    const uint32_t e0 = pl.range_base[key], e1 = pl.range_base[key + 1];
-    const uint32_t ebytes = (e1 - e0) * 4u;  // ranges are multiples of 32 entries
-    const uint32_t sbytes = kStride * 4u;
-    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.bar[b])),
-                 "r"(BLOCK + ebytes + sbytes)
-                 : "memory");
-    bulk(sm.tab[b], e.regmax + (uint64_t)ph * BLOCK, BLOCK, &sm.bar[b]);
-    if (ebytes) bulk(sm.ent[b], pl.entries + e0, ebytes, &sm.bar[b]);
-    bulk(sm.start[b], pl.starts + key * kStride, sbytes, &sm.bar[b]);
-  };
-  if (tid == 0) issue(0);
+  if (w == kW) {  // producer
+    if (lane == 0) {
+      for (uint32_t ph = 0; ph < phases; ++ph) {
+        const int b = ph & 1;
+        // buffer b last held phase ph - 2: wait for its (ph/2 - 1)-th release
+        if (ph >= 2 && !mbar_wait(&sm.empty[b], ((ph >> 1) + 1u) & 1u)) {
+          atomicAdd(err, 1ull);
+          return;
+        }
+        const uint64_t key = (uint64_t)blockIdx.x * phases + ph;
+        const uint32_t e0 = pl.range_base[key], e1 = pl.range_base[key + 1];
+        const uint32_t ebytes = (e1 - e0) * 4u;  // ranges are multiples of 32 entries
+        const uint32_t sbytes = kStride * 4u;
+        const uint32_t fb = smem_u32(&sm.full[b]);
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fb),
+                     "r"(BLOCK + ebytes + sbytes)
+                     : "memory");
+        auto bulk = [&](void *dst, const void *src, uint32_t bytes) {
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+              "[%3];" ::"r"(smem_u32(dst)),
+              "l"(src), "r"(bytes), "r"(fb)
+              : "memory");
+        };
+        bulk(sm.tab[b], e.regmax + (uint64_t)ph * BLOCK, BLOCK);
+        if (ebytes) bulk(sm.ent[b], pl.entries + e0, ebytes);
+        bulk(sm.start[b], pl.starts + key * kStride, sbytes);
+      }
+    }
+    return;
+  }
   uint32_t *acc = sm.acc[w];
   uint32_t *accv = sm.accv[w];
+  const uint32_t L = e.L;
+  const bool hll = e.est == 0u;
   for (uint32_t ph = 0; ph < phases; ++ph) {
     const int b = ph & 1;
-    if (tid == 0 && ph + 1 < phases) issue(ph + 1);  // buffer freed by the sync of phase ph-1
-    const uint32_t parity = (ph >> 1) & 1u;
-    uint32_t done = 0;
-    for (uint32_t spin = 0; !done; ++spin) {
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
-          : "=r"(done)
-          : "r"(smem_u32(&sm.bar[b])), "r"(parity)
-          : "memory");
-      if (spin > (1u << 26)) {  // a lost transfer must not hang the GPU: report and stop
-        if (tid == 0) atomicAdd(err, 1ull);
-        return;
-      }
+    if (!mbar_wait(&sm.full[b], (ph >> 1) & 1u)) {
+      if (lane == 0) atomicAdd(err, 1ull);
+      return;
     }
     const uint8_t *tab = sm.tab[b];
     const uint32_t r0 = sm.start[b][w], r1 = sm.start[b][w + 1];
     const uint32_t *ent = sm.ent[b] + lane;
-#pragma unroll 4
-    for (uint32_t r = r0; r < r1; ++r) {  // one entry per lane per round
-      const uint32_t v = ent[r * 32u];
-      const uint32_t M = tab[v & (BLOCK - 1u)];
-      // one atomic per lane: the zero count or S' (same bank either way)
-      const uint32_t c = e.est == 0u ? 1u << (e.L - M) : M;  // HLL / LogLog, PCSA
+    // one entry per lane per round; ILP rounds' loads are issued before their
+    // atomics (one atomic per lane: the zero count or S', same bank either way)
+    auto add = [&](uint32_t v, uint32_t M) {
+      const uint32_t c = hll ? 1u << (L - M) : M;  // HLL / LogLog, PCSA
       atomicAdd((M == 0u ? accv : acc) + (v >> 16), M == 0u ? 1u : c);
+    };
+    uint32_t r = r0;
+    for (; r + ILP <= r1; r += ILP) {
+      uint32_t v[ILP], M[ILP];
+#pragma unroll
+      for (int j = 0; j < ILP; ++j) v[j] = ent[(r + j) * 32u];
+#pragma unroll
+      for (int j = 0; j < ILP; ++j) M[j] = tab[v[j] & (BLOCK - 1u)];
+#pragma unroll
+      for (int j = 0; j < ILP; ++j) add(v[j], M[j]);
     }
-    __syncthreads();
+    for (; r < r1; ++r) {
+      const uint32_t v = ent[r * 32u];
+      add(v, tab[v & (BLOCK - 1u)]);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(&sm.empty[b])) : "memory");
   }
   pdl_trigger();
   const double g = (double)e.g;
@@ -331,7 +378,7 @@ cudaError_t launch_est(const EstParams &e, const PlanLayout &pl, uint64_t n, dou
   auto kern = outS ? k_estimate_plan<BL, true> : k_estimate_plan<BL, false>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  return launch(kern, dim3(pl.ctas), dim3(kT), smem, s, e, pl, n, out, outS, outV, pl.error);
+  return launch(kern, dim3(pl.ctas), dim3(kT + 32), smem, s, e, pl, n, out, outS, outV, pl.error);
 }
 
 }  // namespace

@@ -35,6 +35,18 @@
 #ifndef PIPE
 #define PIPE 0
 #endif
+#ifndef NOACC
+#define NOACC 0
+#endif
+#ifndef ILP
+#define ILP 0
+#endif
+#ifndef NOTAB
+#define NOTAB 0
+#endif
+#ifndef NOENT
+#define NOENT 0
+#endif
 #ifndef ACC64
 #define ACC64 0
 #endif
@@ -94,14 +106,25 @@ k_plan3(const uint8_t *__restrict__ table, const uint32_t *__restrict__ entries,
     const size_t key = (size_t)blockIdx.x * PHASES + ph;
     const uint32_t e0 = range_base[key], e1 = range_base[key + 1];
     const uint32_t ebytes = (e1 - e0) * 4;
+#if NOTAB
+    const uint32_t tbytes = ph < 2 ? BLOCK : 0;  // experiment: table staged once per buffer
+#else
+    const uint32_t tbytes = BLOCK;
+#endif
+#if NOENT
+    const uint32_t xbytes = ph < 2 ? ebytes : 0;  // experiment: entries staged once per buffer
+#else
+    const uint32_t xbytes = ebytes;
+#endif
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.bar[b])),
-                 "r"(BLOCK + ebytes + STRIDE * 4) : "memory");
-    bulk(sm.tab[b], table + (size_t)ph * BLOCK, BLOCK, &sm.bar[b]);
-    if (ebytes) bulk(sm.ent[b], entries + e0, ebytes, &sm.bar[b]);
+                 "r"(tbytes + xbytes + STRIDE * 4) : "memory");
+    if (tbytes) bulk(sm.tab[b], table + (size_t)ph * BLOCK, BLOCK, &sm.bar[b]);
+    if (xbytes) bulk(sm.ent[b], entries + e0, ebytes, &sm.bar[b]);
     bulk(sm.start[b], starts + key * STRIDE, STRIDE * 4, &sm.bar[b]);
   };
   if (tid == 0) issue(0);
   uint32_t *acc = sm.acc[w];
+  uint32_t sink = 0;
 #if ACC64
   unsigned long long *acc64 = sm.acc64_[w];
   for (int i = lane; i < ACC_W; i += 32) acc64[i] = 0ull;
@@ -134,6 +157,28 @@ k_plan3(const uint8_t *__restrict__ table, const uint32_t *__restrict__ entries,
         M = Mn;
       }
     }
+#elif ATOM && ILP
+    // batches of ILP rounds: all loads first, then the atomics
+    uint32_t r = r0;
+    for (; r + ILP <= r1; r += ILP) {
+      uint32_t v[ILP], M[ILP];
+#pragma unroll
+      for (int j = 0; j < ILP; ++j) v[j] = ent[(r + j) * 32];
+#pragma unroll
+      for (int j = 0; j < ILP; ++j) M[j] = tab[v[j] & (BLOCK - 1)];
+#pragma unroll
+      for (int j = 0; j < ILP; ++j)
+#if NOACC
+        sink += (v[j] >> 16) ^ ((1u << (L - M[j])) + ((uint32_t)(M[j] == 0) << 24));
+#else
+        atomicAdd(&acc[v[j] >> 16], (1u << (L - M[j])) + ((uint32_t)(M[j] == 0) << 24));
+#endif
+    }
+    for (; r < r1; ++r) {
+      const uint32_t v = ent[r * 32];
+      const uint32_t M = tab[v & (BLOCK - 1)];
+      atomicAdd(&acc[v >> 16], (1u << (L - M)) + ((uint32_t)(M == 0) << 24));
+    }
 #elif ATOM
     // shared-memory atomics: no ordering between rounds needed
 #pragma unroll 4
@@ -143,7 +188,7 @@ k_plan3(const uint8_t *__restrict__ table, const uint32_t *__restrict__ entries,
 #if ACC64
       atomicAdd(&acc64[v >> 16], (1ull << (L - M)) + ((unsigned long long)(M == 0) << 40));
 #else
-      atomicAdd(&acc[v >> 16], (1u << (L - M)) + ((uint32_t)(M == 0) << 24));
+      atomicAdd(&acc[(v >> 16) & (NOENT ? 255u : 0xFFFFu)], (1u << (L - M)) + ((uint32_t)(M == 0) << 24));
 #endif
     }
 #else
@@ -159,7 +204,7 @@ k_plan3(const uint8_t *__restrict__ table, const uint32_t *__restrict__ entries,
 #endif
     __syncthreads();
   }
-  unsigned long long t = 0;
+  unsigned long long t = sink;
   for (int i = lane; i < ACC_W; i += 32) t += sm.acc[w][i];
   if (t == 42) *out = t;
 }
@@ -174,7 +219,41 @@ static void schedule(std::vector<Ent> &es, std::vector<uint32_t> &out, int slack
   const int n = (int)es.size();
   int R = std::max(1, (n + 31) / 32 + slack);
   std::vector<std::vector<uint32_t>> rounds(R);
-#if SCHED == 3
+#if SCHED == 4
+  // per round: degree-ordered greedy with bank capacity 1, then 2, then 3
+  // (atomics: a repeated host only costs a conflict)
+  R = std::max(1, (n + 31) / 32);
+  rounds.assign(R, {});
+  {
+    std::vector<Ent> rem(es);
+    for (int r = 0; r < R; ++r) {
+      const int target = std::min<int>(32, ((int)rem.size() + (R - r) - 1) / (R - r));
+      int dt[32] = {0}, da[32] = {0};
+      for (auto &e : rem) { dt[(e.off >> 2) & 31]++; da[e.host & 31]++; }
+      std::vector<int> order(rem.size());
+      for (size_t i = 0; i < rem.size(); ++i) order[i] = (int)i;
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        return dt[(rem[x].off >> 2) & 31] + da[rem[x].host & 31] >
+               dt[(rem[y].off >> 2) & 31] + da[rem[y].host & 31];
+      });
+      std::vector<char> taken(rem.size(), 0);
+      int ut[32] = {0}, ua[32] = {0}, cnt = 0;
+      for (int cap = 1; cap <= 32 && cnt < target; ++cap)
+        for (int i : order) {
+          if (cnt >= target) break;
+          if (taken[i]) continue;
+          const int t = (rem[i].off >> 2) & 31, a = rem[i].host & 31;
+          if (ut[t] < cap && ua[a] < cap) { taken[i] = 1; ut[t]++; ua[a]++; cnt++; }
+        }
+      std::vector<Ent> next;
+      for (size_t i = 0; i < rem.size(); ++i)
+        if (taken[i]) rounds[r].push_back(rem[i].off | (uint32_t)rem[i].host << 16);
+        else next.push_back(rem[i]);
+      rem.swap(next);
+    }
+  }
+  if (false)
+#elif SCHED == 3
   R = std::max(1, (n + 31) / 32);
   rounds.assign(R, {});
   for (int i = 0; i < n; ++i) rounds[i / 32].push_back(es[i].off | (uint32_t)es[i].host << 16);
