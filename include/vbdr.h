@@ -82,9 +82,14 @@ typedef struct {
     /* scan_mode: 0 = default; 1 = plain atomic per pair; 2 = L2 load-check,
      * skip the atomic when the stored value already dominates; 3 = reserved
      * (runs as 1); 4 = L1-cached load-check; 5 = per-block shared-memory
-     * cache of recently updated words in front of the mode-2 check.  All
-     * modes give bit-identical state (stored values only move one way within
-     * a slice). */
+     * cache of recently updated words in front of the mode-2 check (the
+     * default for layout fast; 2 for packed); 6 = binned (layout fast,
+     * n_phys <= 2^26, else runs as 5; measured slower than 5): pairs are
+     * partitioned into per-bucket bins of 2^14 BDRs, then each bucket's
+     * max ranks are formed in shared memory and merged into its stamp words
+     * with coalesced stores (the state buffer grows by the bins, about
+     * 4.5 * min(2 n_phys, 2^27) bytes).  All modes give bit-identical state
+     * (stored values only move one way within a slice). */
     uint32_t scan_mode;
     /* est_lanes: lanes cooperating on one host in vbdr_estimate (1, 2, 4, 8,
      * 16 or 32; 0 = auto).  Tuning only; results are identical. */

@@ -21,6 +21,12 @@ struct DevParams {
   uint32_t A0, A1;
   uint32_t tick;             // T of the open slice
   uint32_t est;              // register estimator: 0 HLL, 1 LogLog, 2 PCSA (packed only)
+  // binned scan (scan_mode 6, layout F): per-bucket record bins
+  uint32_t *bins;            // u32[n_bkt][bcap]: (offset in bucket << 5) | rho
+  uint32_t *bcursor;         // u32[n_bkt] fill counts (zero between chunks)
+  uint32_t bkt_log2;         // BDRs per bucket = 2^bkt_log2
+  uint32_t bcap;             // records per bucket
+  uint64_t bchunk;           // pairs per bin + apply round
 };
 
 // H(x, 2^32, A) = fmix32(x ^ A) (R#6: MurmurHash3 finaliser).

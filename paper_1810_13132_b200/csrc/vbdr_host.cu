@@ -71,7 +71,20 @@ double alpha_of(uint64_t s) {
 struct StateLayout {
   uint32_t b, L, zb, F, W;
   uint64_t off_acc, off_sr, off_drv, off_regmax, bytes;
+  // binned scan (scan_mode 6): bins + cursors, 0 bytes otherwise
+  uint32_t bkt_log2 = 0, bcap = 0;
+  uint64_t bchunk = 0, off_bins = 0, off_bcursor = 0;
 };
+
+// scan_mode 0 = default: 5 for layout F, 2 for layout P; mode 6 (binned)
+// only on request and for pools of at most 2^26 BDRs (4096 buckets), else 5
+// (profiles/r01_scan_modes.txt: binned is slower at caida and 10G).
+uint32_t effective_scan_mode(const vbdr_config &n) {
+  const bool fast = n.layout != VBDR_LAYOUT_PACKED;
+  uint32_t m = n.scan_mode ? n.scan_mode : (fast ? 5u : 2u);
+  if (m == 6 && (!fast || n.n_phys > (1ull << 26))) m = fast ? 5u : 2u;
+  return m;
+}
 
 // Validate a config and lay out the state buffer.  Returns an error text or
 // empty on success.
@@ -83,7 +96,7 @@ std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *p
     n.seed_a1 = 0x5EED0002u;
   }
   if (n.layout > 1) return "layout must be 0 (fast) or 1 (packed)";
-  if (n.scan_mode > 5) return "scan_mode must be 0..5";
+  if (n.scan_mode > 6) return "scan_mode must be 0..6";
   if (n.est_lanes > 32 || (n.est_lanes & (n.est_lanes - 1)))
     return "est_lanes must be 0 or a power of two <= 32";
   if (n.est_pass_log2 > 32) return "est_pass_log2 must be 0..32";
@@ -125,6 +138,18 @@ std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *p
   off = align256(off + 4ull * W * n.n_phys);
   pl->off_regmax = off;
   off = align256(off + n.n_phys);
+  if (effective_scan_mode(n) == 6) {
+    // buckets of 2^14 BDRs (64 KB of ranks in shared memory); chunks of up to
+    // 2 n_phys pairs (<= 2^27); bins sized for the mean load + 12.5 % + 512
+    pl->bkt_log2 = log2u(n.n_phys) < 14 ? log2u(n.n_phys) : 14u;
+    const uint64_t n_bkt = n.n_phys >> pl->bkt_log2;
+    pl->bchunk = 2ull * n.n_phys < (1ull << 27) ? 2ull * n.n_phys : (1ull << 27);
+    pl->bcap = (uint32_t)(pl->bchunk / n_bkt + pl->bchunk / n_bkt / 8 + 512);
+    pl->off_bins = off;
+    off = align256(off + 4ull * n_bkt * pl->bcap);
+    pl->off_bcursor = off;
+    off = align256(off + 4ull * n_bkt);
+  }
   pl->bytes = off;
   pl->b = b;
   pl->L = L;
@@ -154,10 +179,17 @@ vbdr_status check_async(vbdr *h, const char *where) {
 cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // scan_mode 0 picks the default; 3 (warp aggregation) is not built and runs as 1.
+int scan_mode(const vbdr *h);
+
+// kernels one scan call of n pairs launches (mode 6: bin + apply per chunk)
+uint64_t scan_launches(const vbdr *h, uint64_t n) {
+  if (scan_mode(h) != 6) return 1;
+  return 2 * ((n + h->p.bchunk - 1) / h->p.bchunk);
+}
+
 int scan_mode(const vbdr *h) {
-  const uint32_t m0 = h->cfg.scan_mode;
-  // default: 5 for the stamps (fast), 2 for packed words (profiles/r01_scan_modes.txt)
-  const uint32_t m = m0 ? m0 : (h->fast ? 5u : 2u);
+  const uint32_t m = effective_scan_mode(h->cfg);
+  if (m == 6) return h->p.bins ? 6 : 5;
   // mode 5 keys its shared-memory cache by word index: fast needs n_phys < 2^32,
   // packed n_phys <= 2^28 (and W <= 15); otherwise use mode 2
   if (m == 5 && (h->fast ? h->p.n_phys >= (1ull << 32) : (h->p.n_phys > (1ull << 28) || h->p.W > 15)))
@@ -377,6 +409,18 @@ vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, v
   p.A1 = h->cfg.seed_a1;
   p.tick = 1;  // slice t = 0 is open, T = t + 1
   p.est = h->cfg.estimator;
+  if (pl.bcap) {
+    p.bins = reinterpret_cast<uint32_t *>(base + pl.off_bins);
+    p.bcursor = reinterpret_cast<uint32_t *>(base + pl.off_bcursor);
+    p.bkt_log2 = pl.bkt_log2;
+    p.bcap = pl.bcap;
+    p.bchunk = pl.bchunk;
+    if (cudaMemsetAsync(p.bcursor, 0, 4ull * (h->cfg.n_phys >> pl.bkt_log2), S(stream)) !=
+        cudaSuccess) {
+      delete h;
+      return VBDR_ECUDA;
+    }
+  }
   h->alpha_g = alpha_of(h->cfg.m);
   h->alpha_z = alpha_of(h->cfg.n_phys);
   vbdr_info_t &in = h->info;
@@ -433,7 +477,7 @@ vbdr_status vbdr_scan_slice(vbdr_t *h, const uint32_t *d_pairs, uint64_t n_pairs
   const cudaError_t e = vbdr_launch::scan(h->p, h->fast, scan_mode(h), d_pairs, n_pairs,
                                           S(stream));
   if (e != cudaSuccess) return cuda_fail(h, e, "scan launch");
-  h->info.launches += 1;
+  h->info.launches += scan_launches(h, n_pairs);
   return VBDR_OK;
 }
 
@@ -673,7 +717,7 @@ vbdr_status vbdr_scan_slice_host(vbdr_t *h, const uint32_t *h_pairs, uint64_t n_
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, h->ev_copied[slot], 0);
     if (e == cudaSuccess) {
       e = vbdr_launch::scan(h->p, h->fast, scan_mode(h), dst, cnt, cs);
-      h->info.launches += 1;
+      h->info.launches += scan_launches(h, cnt);
     }
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_scanned[slot], cs);
     done += cnt;

@@ -82,7 +82,7 @@ def compare_boundary(pool, ref: oracle.Pool, refs_other, hosts_np, hosts_dev, wi
 
 @pytest.mark.parametrize("layout", ["fast", "packed"])
 @pytest.mark.parametrize("scan_mode,est_lanes,passes", [(1, 0, 0), (2, 1, 0), (4, 8, 10), (1, 32, 0),
-                                                       (4, 2, 7), (0, 0, 11), (5, 4, 0)])
+                                                       (4, 2, 7), (0, 0, 11), (5, 4, 0), (6, 0, 0)])
 def test_tiny_every_boundary(layout, scan_mode, est_lanes, passes):
     """configs[0] 'tiny': 10k pairs/slice, 64 hosts, m=32, 2^12 BDRs, k=4."""
     tr = synth.CONFIGS["tiny"]
@@ -110,7 +110,7 @@ def test_tiny_every_boundary(layout, scan_mode, est_lanes, passes):
                          np.concatenate(slices[max(0, t - 3):t + 1]))
 
 
-@pytest.mark.parametrize("scan_mode", [0, 5])
+@pytest.mark.parametrize("scan_mode", [0, 6])
 @pytest.mark.parametrize("layout", ["fast", "packed"])
 @pytest.mark.parametrize("k,m,n_phys", [(1, 2, 64), (3, 16, 1 << 10), (7, 64, 1 << 14),
                                         (15, 8, 1 << 8), (60, 256, 1 << 16), (300, 4, 1 << 9)])
@@ -191,6 +191,28 @@ def test_order_split_and_duplicates_give_identical_state():
         assert np.array_equal(a.export_regmax(), b.export_regmax())
 
 
+def test_binned_scan_chunks_and_full_bins():
+    """scan_mode 6 (binned): a call larger than one chunk (several bin + apply
+    rounds) and a skewed batch whose records overflow their bin (the direct
+    atomicMax fallback) leave the same state as the atomic scan (mode 5)."""
+    n_phys = 1 << 16
+    a = VBDR(64, 3, n_phys, device=DEV, scan_mode=6)
+    b = VBDR(64, 3, n_phys, device=DEV, scan_mode=5)
+    assert a.info()["state_bytes"] > b.info()["state_bytes"]  # the bins
+    rng = np.random.default_rng(7)
+    for t in range(5):
+        big = rng.integers(0, 2**32, (300_001, 2), dtype=np.uint64).astype(np.uint32)
+        skew = np.tile(big[:3], (40_000, 1))  # 120k records into <= 3 bins
+        for pairs in (big, skew):
+            a.scan_slice(dev_u32(pairs))
+            b.scan_slice(dev_u32(pairs))
+        a.slide()
+        b.slide()
+        assert np.array_equal(a.export_ages(), b.export_ages())
+        assert np.array_equal(a.export_regmax(), b.export_regmax())
+        assert a.export_pool_sums() == b.export_pool_sums()
+
+
 def test_host_buffer_path_matches_device_path():
     """vbdr_scan_slice_host / vbdr_estimate_host (the end-to-end entry points)."""
     tr = synth.CONFIGS["tiny"]
@@ -225,7 +247,7 @@ def test_synth_cuda_twin_matches_numpy():
 
 
 @pytest.mark.parametrize("layout,pass_log2,scan_mode", [("fast", 0, 0), ("packed", 0, 0),
-                                                       ("fast", 20, 5), ("packed", 0, 5)])
+                                                       ("fast", 20, 6), ("packed", 0, 5)])
 def test_caida_full_size(layout, pass_log2, scan_mode):
     """configs[1] 'caida' at full size (5M pairs/slice, 2^22 BDRs, m=128, k=5,
     500k hosts) in the launch configuration bench.py times: every register,
@@ -382,8 +404,9 @@ def test_tick_wraparound(layout):
 
 
 def test_abi_errors():
-    """Argument and state errors are reported synchronously, nothing launched."""
-    pool = VBDR(32, 4, 1 << 12, device=DEV)
+    """Argument and state errors are reported synchronously, nothing launched
+    (scan mode 5: one launch per scan call)."""
+    pool = VBDR(32, 4, 1 << 12, device=DEV, scan_mode=5)
     before = pool.info()["launches"]
     bad = torch.zeros(9, dtype=torch.int32, device=DEV)[1:]  # 4-byte aligned only
     with pytest.raises(RuntimeError, match="EINVAL"):
