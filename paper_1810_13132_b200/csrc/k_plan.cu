@@ -207,6 +207,97 @@ __global__ void __launch_bounds__(kT) k_plan_pad(BuildArgs a) {
   }
 }
 
+// One block per key, warp w re-orders group w's entries round by round so a
+// round touches each shared-memory bank of the table (register offset) and of
+// the accumulators (host lane) as few times as possible: round r takes
+// ceil(remaining / rounds left) entries, first with at most one entry per
+// bank on either side, then two, ... (greedy, warp-parallel: per 32-entry
+// chunk the lowest lane of each bank wins).  Only the order changes, never
+// the entries, so the sums are unchanged; it cuts bank-conflict wavefronts
+// in k_estimate_plan.  Keys over the stage capacity are left alone (the
+// plan is refused anyway).
+__global__ void __launch_bounds__(kT) k_plan_sched(BuildArgs a, const uint32_t *range_size) {
+  __shared__ uint32_t E[kCap];        // the key's entries: per group the remaining list
+  __shared__ uint32_t cnt[kW][64];    // per warp: table-bank [0, 32) and acc-bank [32, 64) use
+  const uint64_t key = blockIdx.x;
+  const uint32_t total = range_size[key];
+  if (total > (uint32_t)kCap) return;
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  uint32_t *ent = a.entries + a.range_base[key];
+  for (uint32_t i = threadIdx.x; i < total; i += kT) E[i] = ent[i];
+  __syncthreads();
+  const uint32_t r0 = a.starts[key * kStride + w], R = a.starts[key * kStride + w + 1] - r0;
+  uint32_t *L = E + 32u * r0;  // this warp's list
+  uint32_t *out = ent + 32u * r0;
+  constexpr uint32_t kTrash = (uint32_t)kSlots * 32u;  // accumulator indices >= this are padding
+  constexpr uint32_t kTaken = 0xFFFFFFFFu;
+  // drop the padding: compact the real entries to the front
+  uint32_t rem = 0;
+  for (uint32_t c = 0; c < 32u * R; c += 32u) {
+    const uint32_t v = L[c + lane];
+    const bool real = (v >> 16) < kTrash;
+    const uint32_t m = __ballot_sync(0xffffffffu, real);
+    __syncwarp();
+    if (real) L[rem + __popc(m & ((1u << lane) - 1u))] = v;
+    rem += __popc(m);
+    __syncwarp();
+  }
+  for (uint32_t r = 0; r < R; ++r) {
+    const uint32_t target = min(32u, (rem + (R - r) - 1u) / (R - r));
+    cnt[w][lane] = 0u;
+    cnt[w][32 + lane] = 0u;
+    __syncwarp();
+    uint32_t taken = 0, mine = 0;  // lane j ends up holding the entry of round lane j
+    for (uint32_t cap = 1; taken < target; ++cap) {
+      for (uint32_t c = 0; c < rem && taken < target; c += 32u) {
+        const uint32_t idx = c + lane;
+        const uint32_t v = idx < rem ? L[idx] : kTaken;
+        const uint32_t tb = (v >> 2) & 31u, ab = (v >> 16) & 31u;
+        bool cand = v != kTaken && cnt[w][tb] < cap && cnt[w][32 + ab] < cap;
+        const uint32_t cm = __ballot_sync(0xffffffffu, cand);
+        // lowest candidate lane per table bank and per accumulator bank
+        const uint32_t mt = __match_any_sync(0xffffffffu, cand ? tb : 64u + lane) & cm;
+        const uint32_t ma = __match_any_sync(0xffffffffu, cand ? ab : 64u + lane) & cm;
+        cand = cand && (mt & ((1u << lane) - 1u)) == 0u && (ma & ((1u << lane) - 1u)) == 0u;
+        const uint32_t am = __ballot_sync(0xffffffffu, cand);
+        const uint32_t rank = __popc(am & ((1u << lane) - 1u));
+        const bool acc = cand && taken + rank < target;
+        const uint32_t got = __ballot_sync(0xffffffffu, acc);
+        if (acc) {
+          cnt[w][tb] += 1u;
+          cnt[w][32 + ab] += 1u;
+          L[idx] = kTaken;
+        }
+        // hand each accepted entry to the lane of its round slot
+#pragma unroll 1
+        for (uint32_t m = got; m; m &= m - 1u) {
+          const uint32_t src = __ffs(m) - 1u;
+          const uint32_t val = __shfl_sync(0xffffffffu, v, src);
+          if (lane == taken) mine = val;
+          ++taken;
+        }
+        __syncwarp();
+      }
+    }
+    // pad the round; lane j's padding uses lane j's trash accumulator
+    if (lane >= taken) mine = (kTrash + lane) << 16;
+    out[32u * r + lane] = mine;
+    // drop the taken entries from the list
+    uint32_t n2 = 0;
+    for (uint32_t c = 0; c < rem; c += 32u) {
+      const uint32_t idx = c + lane;
+      const uint32_t v = idx < rem ? L[idx] : kTaken;
+      const bool keep = v != kTaken;
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();
+      if (keep) L[n2 + __popc(m & ((1u << lane) - 1u))] = v;
+      n2 += __popc(m);
+      __syncwarp();
+    }
+    rem = n2;
+  }
+}
+
 // --------------------------------------------------------------- estimate
 __device__ __forceinline__ double hll_finish(double agg, double D, double lc, uint64_t V,
                                              double s) {
@@ -414,6 +505,7 @@ cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, 
   k_plan_bases<<<1, 1024, 0, s>>>(a, range_size_scratch, nkeys);
   k_plan_fill<<<grid ? grid : 1, 256, 0, s>>>(a);
   k_plan_pad<<<(uint32_t)nkeys, kT, 0, s>>>(a);
+  k_plan_sched<<<(uint32_t)nkeys, kT, 0, s>>>(a, range_size_scratch);
   return cudaGetLastError();
 }
 

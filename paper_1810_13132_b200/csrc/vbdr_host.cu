@@ -594,7 +594,7 @@ vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts
     e = cudaMemcpyAsync(&max_range, pl.max_range, 4, cudaMemcpyDeviceToHost, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e != cudaSuccess) return cuda_fail(h, e, "plan_build");
-  h->info.launches += 5;
+  h->info.launches += 6;
   if (max_range > (uint32_t)vbdr_launch::kPlanEntCap) {
     h->plans.erase(d_plan);
     return fail(h, VBDR_ERANGE, "a register block holds more entries than shared memory stages");
