@@ -80,8 +80,9 @@ typedef struct {
     /* layout: vbdr_layout. */
     uint32_t layout;
     /* scan_mode: 0 = default; 1 = plain atomic per pair; 2 = L2 load-check,
-     * skip the atomic when the stored value already dominates; 3 = reserved
-     * (runs as 1); 4 = L1-cached load-check; 5 = per-block shared-memory
+     * skip the atomic when the stored value already dominates; 3 = warp-
+     * aggregated atomic (lanes with the same word combine their update,
+     * one lane checks L2 and issues it); 4 = L1-cached load-check; 5 = per-block shared-memory
      * cache of recently updated words in front of the mode-2 check (the
      * default for layout fast; 2 for packed); 6 = binned (layout fast,
      * n_phys <= 2^26, else runs as 5; measured slower than 5): pairs are

@@ -84,6 +84,18 @@ __device__ __forceinline__ void record(uint32_t aip, uint32_t bip, const DevPara
       cache_put(cache, key, val);
       return;
     }
+    if constexpr (MODE == 3) {
+      // warp-aggregated atomicMax (north star): lanes hitting the same BDR
+      // combine their ranks with a max reduction, the lowest of them checks
+      // L2 (as mode 2) and issues the one atomic
+      const uint32_t live = __activemask();
+      const uint32_t peers = __match_any_sync(live, pidx);
+      const uint32_t m = __reduce_max_sync(peers, val);
+      if ((threadIdx.x & 31u) != (uint32_t)(__ffs(peers) - 1)) return;
+      if (ld_relaxed(a) >= m) return;
+      atomicMax(a, m);
+      return;
+    }
     if constexpr (MODE == 2) {
       if (ld_relaxed(a) >= val) return;  // stored value dominates: max is a no-op
     }
@@ -112,6 +124,17 @@ __device__ __forceinline__ void record(uint32_t aip, uint32_t bip, const DevPara
         if (((cur >> (ZB * g)) & S::FM) == 0u) zero |= S::FM << (ZB * g);
       if ((cur & fm) != 0u) atomicAnd(a, ~fm);
       cache_put(cache, key, zero | fm);
+      return;
+    }
+    if constexpr (MODE == 3) {
+      // warp-aggregated SetDR: lanes hitting the same word OR their field
+      // masks, the lowest of them checks L2 and issues the one atomicAnd
+      const uint32_t live = __activemask();
+      const uint32_t peers = __match_any_sync(live, (unsigned long long)(uintptr_t)a);
+      const uint32_t m = __reduce_or_sync(peers, fm);
+      if ((threadIdx.x & 31u) != (uint32_t)(__ffs(peers) - 1)) return;
+      if ((ld_relaxed(a) & m) == 0u) return;
+      atomicAnd(a, ~m);
       return;
     }
     if constexpr (MODE == 2) {
@@ -643,6 +666,9 @@ cudaError_t launch_scan(const DevParams &p, int mode, const uint4 *pairs2, uint6
   switch (mode) {
     case 2:
       return launch(k_scan<FAST, ZB, 2>, grid_for(k_scan<FAST, ZB, 2>, work, T), T, 0, s, pairs2,
+                    n2, tail, p);
+    case 3:
+      return launch(k_scan<FAST, ZB, 3>, grid_for(k_scan<FAST, ZB, 3>, work, T), T, 0, s, pairs2,
                     n2, tail, p);
     case 4:
       return launch(k_scan<FAST, ZB, 4>, grid_for(k_scan<FAST, ZB, 4>, work, T), T, 0, s, pairs2,

@@ -178,7 +178,7 @@ vbdr_status check_async(vbdr *h, const char *where) {
 
 cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// scan_mode 0 picks the default; 3 (warp aggregation) is not built and runs as 1.
+// scan_mode 0 picks the default (effective_scan_mode).
 int scan_mode(const vbdr *h);
 
 // kernels one scan call of n pairs launches (mode 6: bin + apply per chunk)
@@ -194,7 +194,7 @@ int scan_mode(const vbdr *h) {
   // packed n_phys <= 2^28 (and W <= 15); otherwise use mode 2
   if (m == 5 && (h->fast ? h->p.n_phys >= (1ull << 32) : (h->p.n_phys > (1ull << 28) || h->p.W > 15)))
     return 2;
-  return m == 3 ? 1 : (int)m;
+  return (int)m;
 }
 
 vbdr_launch::EstParams est_params(const vbdr *h) {

@@ -82,7 +82,8 @@ def compare_boundary(pool, ref: oracle.Pool, refs_other, hosts_np, hosts_dev, wi
 
 @pytest.mark.parametrize("layout", ["fast", "packed"])
 @pytest.mark.parametrize("scan_mode,est_lanes,passes", [(1, 0, 0), (2, 1, 0), (4, 8, 10), (1, 32, 0),
-                                                       (4, 2, 7), (0, 0, 11), (5, 4, 0), (6, 0, 0)])
+                                                       (4, 2, 7), (0, 0, 11), (5, 4, 0), (6, 0, 0),
+                                                       (3, 16, 0)])
 def test_tiny_every_boundary(layout, scan_mode, est_lanes, passes):
     """configs[0] 'tiny': 10k pairs/slice, 64 hosts, m=32, 2^12 BDRs, k=4."""
     tr = synth.CONFIGS["tiny"]
@@ -110,7 +111,7 @@ def test_tiny_every_boundary(layout, scan_mode, est_lanes, passes):
                          np.concatenate(slices[max(0, t - 3):t + 1]))
 
 
-@pytest.mark.parametrize("scan_mode", [0, 6])
+@pytest.mark.parametrize("scan_mode", [0, 3, 6])
 @pytest.mark.parametrize("layout", ["fast", "packed"])
 @pytest.mark.parametrize("k,m,n_phys", [(1, 2, 64), (3, 16, 1 << 10), (7, 64, 1 << 14),
                                         (15, 8, 1 << 8), (60, 256, 1 << 16), (300, 4, 1 << 9)])
