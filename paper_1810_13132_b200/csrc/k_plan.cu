@@ -33,6 +33,12 @@ using vbdr_launch::PlanLayout;
 
 namespace {
 
+#ifndef VBDR_PLAN_PREFETCH
+#define VBDR_PLAN_PREFETCH 1  // phases ahead (0 = off; profiles/r01_plan_variants.txt)
+#endif
+#ifndef VBDR_PLAN_PREFETCH_TAB
+#define VBDR_PLAN_PREFETCH_TAB 0
+#endif
 #ifndef VBDR_PLAN_SORT
 #define VBDR_PLAN_SORT 0
 #endif
@@ -397,6 +403,24 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
         bulk(sm.tab[b], e.regmax + (uint64_t)ph * BLOCK, BLOCK);
         if (ebytes) bulk(sm.ent[b], pl.entries + e0, ebytes);
         bulk(sm.start[b], pl.starts + key * kStride, sbytes);
+#if VBDR_PLAN_PREFETCH
+        // warm L2 with a later phase's entries (streamed from DRAM once): the
+        // stage refill then waits on L2, not DRAM, latency
+        const uint32_t pf = ph + VBDR_PLAN_PREFETCH;
+        if (pf < phases) {
+          const uint64_t k2 = (uint64_t)blockIdx.x * phases + pf;
+          const uint32_t f0 = pl.range_base[k2], f1 = pl.range_base[k2 + 1];
+          if (f1 > f0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pl.entries + f0),
+                         "r"((f1 - f0) * 4u)
+                         : "memory");
+#if VBDR_PLAN_PREFETCH_TAB
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(e.regmax + (uint64_t)pf * BLOCK),
+                       "r"(BLOCK)
+                       : "memory");
+#endif
+        }
+#endif
       }
     }
     return;
