@@ -161,7 +161,7 @@ cudaError_t run(const EstParams &e, const uint32_t *hosts, uint64_t n, double *o
     const uint64_t need = (n * G + kThreads - 1) / kThreads;
     const uint64_t grid = need < resident ? need : resident;
     for (uint32_t p = 0; p < passes; ++p) {
-      const cudaError_t err = launch(kern, dim3((uint32_t)(grid ? grid : 1)), dim3(kThreads), smem,
+      const cudaError_t err = launch_ex(pdl_mode() == 1, kern, dim3((uint32_t)(grid ? grid : 1)), dim3(kThreads), smem,
                                      s, e, hosts, n, out, outS, outV, p, p + 1 == passes);
       if (err != cudaSuccess) return err;
     }
@@ -179,7 +179,7 @@ cudaError_t run(const EstParams &e, const uint32_t *hosts, uint64_t n, double *o
   const uint64_t resident = (uint64_t)per_sm * sm_count();
   const uint64_t need = (n * G + kThreads - 1) / kThreads;
   const uint64_t grid = need < resident ? need : resident;
-  return launch(kern, dim3((uint32_t)(grid ? grid : 1)), dim3(kThreads), smem, s, e, hosts, n, out,
+  return launch_ex(pdl_mode() == 1, kern, dim3((uint32_t)(grid ? grid : 1)), dim3(kThreads), smem, s, e, hosts, n, out,
                 outS, outV, 0u, true);
 }
 

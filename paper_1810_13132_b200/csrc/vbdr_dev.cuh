@@ -107,31 +107,29 @@ struct WMax {
 // kernel calls pdl_wait() before its first global-memory access, which blocks
 // until the predecessor grid has completed and its writes are visible -- the
 // same ordering as a plain launch, minus the launch gap.
-// Off by default: +1.7 % at caida but -20 % at 10G, where dependent CTAs
-// scheduled early unbalance the persistent grids (profiles/r01_pdl.txt).
-#ifndef VBDR_PDL
-#define VBDR_PDL 0
-#endif
-
+// The device side is always compiled in (griddepcontrol.wait is a no-op in a
+// grid launched without the attribute); whether a launch sets the attribute
+// is decided at run time (pdl_mode below, env VBDR_PDL: 0 off, 1 every
+// launch, unset = every launch except the gather estimate, where early
+// dependent CTAs unbalance the persistent grid: profiles/r01_pdl.txt).
 __device__ __forceinline__ void pdl_wait() {
-#if VBDR_PDL
   asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
 }
 
 __device__ __forceinline__ void pdl_trigger() {
-#if VBDR_PDL
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
 }
 
+// 0 off, 1 on for every launch, 2 (default) on except the gather estimate
+int pdl_mode();
+
 template <typename... KArgs, typename... Args>
-cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                   Args... args) {
+cudaError_t launch_ex(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = VBDR_PDL;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
@@ -139,6 +137,12 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args... args) {
+  return launch_ex(pdl_mode() != 0, kern, grid, block, smem, s, args...);
 }
 
 }  // namespace vbdr_dev

@@ -12,6 +12,7 @@
 
 #include "../../include/vbdr.h"
 #include "vbdr_dev.cuh"
+#include <cstdlib>
 
 using vbdr_dev::DevParams;
 
@@ -30,6 +31,17 @@ struct vbdr {
   cudaEvent_t ev_hosts_in = nullptr;    // host ids copied (copy stream)
   cudaEvent_t ev_hosts_free = nullptr;  // last estimate that read the host stage
 };
+
+namespace vbdr_dev {
+int pdl_mode() {
+  static const int mode = [] {
+    const char *v = std::getenv("VBDR_PDL");
+    if (!v || !*v) return 2;
+    return v[0] == '0' ? 0 : (v[0] == '1' ? 1 : 2);
+  }();
+  return mode;
+}
+}  // namespace vbdr_dev
 
 namespace {
 
