@@ -35,6 +35,9 @@
 #ifndef PIPE
 #define PIPE 0
 #endif
+#ifndef WORDLD
+#define WORDLD 0
+#endif
 #ifndef NOACC
 #define NOACC 0
 #endif
@@ -59,14 +62,18 @@
 #ifndef SYNCW
 #define SYNCW 1
 #endif
-constexpr int THREADS = 512, WARPS = THREADS / 32, SLOTS = 7, BLOCK = 1 << BLOCK_LOG2;
+#ifndef THREADS_
+#define THREADS_ 512
+#define SLOTS_ 7
+#endif
+constexpr int THREADS = THREADS_, WARPS = THREADS / 32, SLOTS = SLOTS_, BLOCK = 1 << BLOCK_LOG2;
 constexpr int PHASES = (1 << 22) / BLOCK;
 constexpr int ACC_W = SLOTS * 32 + 32;  // per warp: 224 host slots + 32 trash lanes
 #ifndef ENT_CAP_
 #define ENT_CAP_ (BLOCK_LOG2 == 16 ? 8192 : 4608)
 #endif
 constexpr int ENT_CAP = ENT_CAP_;
-constexpr int STRIDE = 20;  // warp round starts per key (17 used), 16-byte padded
+constexpr int STRIDE = (WARPS + 4) / 4 * 4;  // warp round starts per key (WARPS + 1 used), 16-byte padded
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -164,8 +171,16 @@ k_plan3(const uint8_t *__restrict__ table, const uint32_t *__restrict__ entries,
       uint32_t v[ILP], M[ILP];
 #pragma unroll
       for (int j = 0; j < ILP; ++j) v[j] = ent[(r + j) * 32];
+#if WORDLD
+#pragma unroll
+      for (int j = 0; j < ILP; ++j) {
+        const uint32_t o = v[j] & (BLOCK - 1);
+        M[j] = (reinterpret_cast<const uint32_t *>(tab)[o >> 2] >> ((o & 3) * 8)) & 0xFFu;
+      }
+#else
 #pragma unroll
       for (int j = 0; j < ILP; ++j) M[j] = tab[v[j] & (BLOCK - 1)];
+#endif
 #pragma unroll
       for (int j = 0; j < ILP; ++j)
 #if NOACC
