@@ -95,7 +95,7 @@ __device__ __forceinline__ void locate_entry(const BuildArgs &a, uint64_t h, uin
 #else
   bank = (off >> 2) & 31u;  // register bank in the staged block
 #endif
-  val = off | ((slot * 32u + lane) << 16);
+  val = off | ((slot * 32u + lane) << 18);  // accumulator byte offset << 16
 }
 
 __global__ void k_plan_count(BuildArgs a) {
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kT) k_plan_pad(BuildArgs a) {
   const uint32_t r0 = a.starts[key * kStride + w], R = a.starts[key * kStride + w + 1] - r0;
   for (uint32_t i = n_w + lane; i < 32u * R; i += 32u) {
     const uint32_t pos = stripe(i, R);
-    a.entries[a.range_base[key] + 32u * r0 + pos] = (uint32_t)(kSlots * 32 + (pos & 31u)) << 16;
+    a.entries[a.range_base[key] + 32u * r0 + pos] = (uint32_t)(kSlots * 32 + (pos & 31u)) << 18;
   }
 }
 
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kT) k_plan_sched(BuildArgs a, const uint32_t *
   uint32_t rem = 0;
   for (uint32_t c = 0; c < 32u * R; c += 32u) {
     const uint32_t v = L[c + lane];
-    const bool real = (v >> 16) < kTrash;
+    const bool real = (v >> 18) < kTrash;
     const uint32_t m = __ballot_sync(0xffffffffu, real);
     __syncwarp();
     if (real) L[rem + __popc(m & ((1u << lane) - 1u))] = v;
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kT) k_plan_sched(BuildArgs a, const uint32_t *
       for (uint32_t c = 0; c < rem && taken < target; c += 32u) {
         const uint32_t idx = c + lane;
         const uint32_t v = idx < rem ? L[idx] : kTaken;
-        const uint32_t tb = (v >> 2) & 31u, ab = (v >> 16) & 31u;
+        const uint32_t tb = (v >> 2) & 31u, ab = (v >> 18) & 31u;
         bool cand = v != kTaken && cnt[w][tb] < cap && cnt[w][32 + ab] < cap;
         const uint32_t cm = __ballot_sync(0xffffffffu, cand);
         // lowest candidate lane per table bank and per accumulator bank
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kT) k_plan_sched(BuildArgs a, const uint32_t *
       }
     }
     // pad the round; lane j's padding uses lane j's trash accumulator
-    if (lane >= taken) mine = (kTrash + lane) << 16;
+    if (lane >= taken) mine = (kTrash + lane) << 18;
     out[32u * r + lane] = mine;
     // drop the taken entries from the list
     uint32_t n2 = 0;
@@ -317,8 +317,9 @@ struct __align__(128) PlanSmem {
   uint8_t tab[2][1 << BLOCK_LOG2];
   uint32_t ent[2][kCap];
   uint32_t start[2][kStride];
-  uint32_t acc[kW][kAccW];   // S' = sum over M >= 1 of 2^(L - M) (HLL) or M
-  uint32_t accv[kW][kAccW];  // V = number of M == 0
+  // per warp: [0, kAccW) S' = sum over M >= 1 of 2^(L - M) (HLL) or M;
+  // [kAccW, 2 kAccW) the zero count, V 2^L (HLL, mod 2^32) or V
+  uint32_t acc[kW][2 * kAccW];
   uint64_t full[2];          // TMA bytes of buffer b landed
   uint64_t empty[2];         // all kW consumer warps are done with buffer b
   double etot_z;
@@ -340,7 +341,7 @@ __device__ __forceinline__ bool mbar_wait(uint64_t *bar, uint32_t parity) {
 // kW consumer warps + one producer warp (TMA issue only).  Buffers are
 // handed over with full / empty mbarriers, so a warp that finishes a block
 // early starts on the next one instead of waiting at a CTA barrier.
-template <int BLOCK_LOG2, bool SUMS>
+template <int BLOCK_LOG2, bool SUMS, bool HLL>
 __global__ void __launch_bounds__(kT + 32, 1)
 k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out,
                 unsigned long long *__restrict__ outS, uint32_t *__restrict__ outV,
@@ -354,7 +355,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
   if (w < kW) {
     for (int i = lane; i < kAccW; i += 32) {
       sm.acc[w][i] = 0u;
-      sm.accv[w][i] = 0u;
+      sm.acc[w][kAccW + i] = 0u;
     }
   }
   if (tid == 0) {
@@ -426,9 +427,9 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
     return;
   }
   uint32_t *acc = sm.acc[w];
-  uint32_t *accv = sm.accv[w];
-  const uint32_t L = e.L;
-  const bool hll = e.est == 0u;
+  uint32_t *accv = acc + kAccW;
+  const uint32_t acc_base = smem_u32(acc);
+  const uint32_t K = 1u << e.L;  // 2^(L - M) = K >> M
   for (uint32_t ph = 0; ph < phases; ++ph) {
     const int b = ph & 1;
     if (!mbar_wait(&sm.full[b], (ph >> 1) & 1u)) {
@@ -440,9 +441,12 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
     const uint32_t *ent = sm.ent[b] + lane;
     // one entry per lane per round; ILP rounds' loads are issued before their
     // atomics (one atomic per lane: the zero count or S', same bank either way)
+    // one atomic per lane: M >= 1 adds its term to S', M = 0 adds to the
+    // zero count (2^L for HLL, so both are one shift; same bank either way)
     auto add = [&](uint32_t v, uint32_t M) {
-      const uint32_t c = hll ? 1u << (L - M) : M;  // HLL / LogLog, PCSA
-      atomicAdd((M == 0u ? accv : acc) + (v >> 16), M == 0u ? 1u : c);
+      const uint32_t c = HLL ? K >> M : (M == 0u ? 1u : M);
+      const uint32_t addr = acc_base + (v >> 16) + (M == 0u ? 4u * kAccW : 0u);
+      asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(c) : "memory");
     };
     uint32_t r = r0;
     for (; r + ILP <= r1; r += ILP) {
@@ -467,9 +471,11 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
   for (int s = 0; s < kSlots; ++s) {
     const uint64_t h = slot_host(blockIdx.x, w, lane, s, gridDim.x);
     if (h >= n) break;
-    const uint32_t V = accv[s * 32 + lane];
-    const unsigned long long S =
-        acc[s * 32 + lane] + (e.est == 0u ? (unsigned long long)V << e.L : 0ull);
+    const uint32_t Sp = acc[s * 32 + lane], Vz = accv[s * 32 + lane];
+    // HLL: Vz = V 2^L mod 2^32, which wraps only for V = g when g 2^L = 2^32,
+    // i.e. every register zero -- exactly when S' = 0 (each M >= 1 adds >= 1)
+    const uint32_t V = HLL ? (Sp == 0u ? e.g : Vz >> e.L) : Vz;
+    const unsigned long long S = Sp + (HLL ? (unsigned long long)V << e.L : 0ull);
     if constexpr (SUMS) {
       outS[h] = S;
       outV[h] = V;
@@ -490,7 +496,8 @@ template <int BL>
 cudaError_t launch_est(const EstParams &e, const PlanLayout &pl, uint64_t n, double *out,
                        unsigned long long *outS, uint32_t *outV, cudaStream_t s) {
   const size_t smem = sizeof(PlanSmem<BL>);
-  auto kern = outS ? k_estimate_plan<BL, true> : k_estimate_plan<BL, false>;
+  auto kern = outS ? (e.est == 0u ? k_estimate_plan<BL, true, true> : k_estimate_plan<BL, true, false>)
+                   : (e.est == 0u ? k_estimate_plan<BL, false, true> : k_estimate_plan<BL, false, false>);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   return launch(kern, dim3(pl.ctas), dim3(kT + 32), smem, s, e, pl, n, out, outS, outV, pl.error);
