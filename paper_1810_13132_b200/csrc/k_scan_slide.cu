@@ -38,6 +38,9 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
 // L1-to-L2 request slots that bound the scan.  An entry
 // is inserted only after its atomic was issued (or a load saw the value), so
 // it never exceeds what global memory will hold when the kernel ends.
+#ifndef VBDR_SCAN_DIRECT_RHO
+#define VBDR_SCAN_DIRECT_RHO 0
+#endif
 #ifndef VBDR_SCAN_CACHE_SLOTS
 #define VBDR_SCAN_CACHE_SLOTS 2048  // 16 KB per block
 #endif
@@ -75,6 +78,13 @@ __device__ __forceinline__ void record(uint32_t aip, uint32_t bip, const DevPara
     if constexpr (MODE == 5) {
       const uint32_t key = pidx + 1u;  // n_phys < 2^32 for this mode
       if (cache_hit(cache, key, val, true)) return;
+#if VBDR_SCAN_DIRECT_RHO
+      if (rho >= VBDR_SCAN_DIRECT_RHO) {  // high ranks rarely lose: skip the check
+        atomicMax(a, val);
+        cache_put(cache, key, val);
+        return;
+      }
+#endif
       const uint32_t cur = ld_relaxed(a);
       if (cur >= val) {
         cache_put(cache, key, cur);
