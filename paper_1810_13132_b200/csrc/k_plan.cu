@@ -7,23 +7,26 @@
 // from shared memory instead:
 //   * a PLAN, built once per host list, assigns every host to an accumulator
 //     slot of one warp of one of `ctas` persistent CTAs, spreading hosts over
-//     CTAs first, then warps, then lanes (host_slot below), and lists, for
-//     every (CTA, register block of 2^16)
-//     phase and every warp, the warp's (host, i) gathers that fall in that
-//     block (Alg.5 / Alg.3 indices, precomputed) as ROUNDS of 32 entries
-//     (offset in block | accumulator index << 16), one entry per lane.  Any
-//     lane may serve any of its warp's hosts, so all lanes stay busy (a
-//     thread-owns-its-hosts layout idles ~35 % of the lanes on the longest
-//     run); within a group the entries are ordered by shared-memory bank of
-//     their register and striped over the rounds (sorted index i -> round
-//     i mod R, lane i / R), so one round touches each bank about once;
+//     CTAs first, then warps, then lanes (slot_host below), and lists, for
+//     every (CTA, register block of 2^16) phase and every warp, the warp's
+//     (host, i) gathers that fall in that block (Alg.5 / Alg.3 indices,
+//     precomputed) as ROUNDS of 32 entries (offset in block | accumulator
+//     byte offset << 16), one entry per lane.  Any lane may serve any of its
+//     warp's hosts, so all lanes stay busy (a thread-owns-its-hosts layout
+//     idles ~35 % of the lanes on the longest run).  The entries of a group
+//     are first striped over its rounds by shared-memory bank of their
+//     register (k_plan_fill), then re-ordered so each round touches every
+//     bank -- register side and accumulator side -- as few times as possible
+//     (k_plan_sched);
 //   * per slice, each CTA streams the register array through shared memory
-//     one 64 KB block at a time (TMA bulk copies, double buffered, mbarrier),
-//     together with its entries for that block, and every lane adds
+//     one 64 KB block at a time (TMA bulk copies issued by a producer warp,
+//     two stages, full / empty mbarriers, the next block's entries prefetched
+//     into L2), together with its entries for that block, and every lane adds
 //     2^(L - M) for M >= 1 (M for LogLog/PCSA) into the entry's u32
-//     accumulator with a shared-memory atomic, and counts M == 0 in a second
-//     array (S = S' + V 2^L; S' <= g 2^(L-1) = 2^31 for L = 32 - log2 g)
-//     -- no L2 gathers.  The last step is the fp64 finish of k_estimate.
+//     accumulator with a shared-memory atomic, or 2^L (1) into the host's
+//     zero count for M = 0 (S = S' + V 2^L; S' <= g 2^(L-1) = 2^31 for
+//     L = 32 - log2 g) -- no L2 gathers.  The last step is the fp64 finish
+//     of k_estimate.
 // Integer sums make the result bit-identical to the gather kernel.
 #include "vbdr_dev.cuh"
 
@@ -40,7 +43,7 @@ namespace {
 #define VBDR_PLAN_PREFETCH_TAB 0
 #endif
 #ifndef VBDR_PLAN_SORT
-#define VBDR_PLAN_SORT 0
+#define VBDR_PLAN_SORT 0  // fill order: 0 register bank, 1 accumulator bank, 2 both (experiment)
 #endif
 
 constexpr int kT = vbdr_launch::kPlanThreads;   // 512
