@@ -2,8 +2,9 @@
 """bench.py -- the VBDR hot path on B200 (one JSON line on rank 0).
 
 A step is one slice of the method over one batch of synthetic input:
-    vbdr_scan_slice (Np pairs) -> [N>1: allreduce(MAX) merge] -> vbdr_slide
-    -> vbdr_estimate (all H hosts)
+    vbdr_scan_slice (Np pairs) -> [N>1: merge] -> vbdr_slide
+    -> estimate of all H hosts (vbdr_estimate_plan with a plan built once
+       before the timed region when the pool allows one, else vbdr_estimate)
 on BASELINE.json configs[1] ('caida': 5M pairs/slice, 500k Zipf hosts, m=128,
 2^22 physical BDRs, k=5) unless --config says otherwise.
 
@@ -11,8 +12,12 @@ value   = pairs/s of whole steps (Mpairs/s), inputs resident in HBM, L2 flushed
           before every step, device time from CUDA events, max over ranks.
 e2e     = the same through the host-buffer C ABI entry points (pinned host pairs
           copied in, estimates copied out, inside the timed region).
-Under torchrun (N>1) each rank scans 1/N of every slice's pairs, the stamp
-arrays merge by NCCL allreduce(MAX), and each rank estimates 1/N of the hosts.
+Under torchrun (N>1) each rank scans 1/N of every slice's pairs and the
+ranks merge their slice ranks before the slide (--merge: default "sharded" =
+NCCL reduce-scatter(MAX) of the u8 per-BDR ranks, a sharded slide, an
+all-gather of the register shards and an all-reduce of the pool sums;
+"stamps" = allreduce(MAX) of the stamp words; "delta"; "p2p" = the fused
+peer-memory merge+slide); each rank estimates 1/N of the hosts.
 
 --impl reference times the oracle (oracle/, single thread, host cores) on a
 1/32-scale replica of the same workload; rank 0 only.
