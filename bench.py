@@ -45,6 +45,7 @@ FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
 WORKLOADS = {
     "tiny": dict(m=32, k=4, n_phys=1 << 12),
     "caida": dict(m=128, k=5, n_phys=1 << 22),
+    "caida_bursty": dict(m=128, k=5, n_phys=1 << 22),  # caida with packet trains
     "10G": dict(m=256, k=10, n_phys=1 << 26),
     "bigwin": dict(m=256, k=60, n_phys=1 << 28),
 }

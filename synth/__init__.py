@@ -18,6 +18,13 @@ available offline).  Pair ``i`` of slice ``t`` under ``seed``:
            (y & 0xFFFFFFFF) mod U[h]     otherwise              (persistent universe)
     bip  = lowbias32(((h * 0x9E3779B1 + v) mod 2^32) ^ 0x3C3C3C3C)
 
+Bursty variant (``burst`` > 0, SURVEY.md section 8 d.3 "packet trains"):
+position ``j`` continues the train of ``j - 1`` when bit 63 of
+``sm64(x_j ^ 0xD1B54A32D192ED03)`` is set (probability 1/2), for at most
+``burst - 1`` steps back; pair ``i`` is then the i.i.d. pair of the train's
+first position, so trains have length 1 + Geom(1/2) (capped at ``burst``)
+and any range of positions can still be generated independently.
+
 ``cdf`` (fp64, Zipf weights (h+1)^-s, last entry forced to 1.0) and ``U``
 (u32 universe sizes max(1, floor(U0 (h+1)^-s))) are tables built once here with
 numpy and handed to both the numpy twin and the CUDA kernel
@@ -69,6 +76,7 @@ class TraceConfig:
     zipf_s: float = 1.1
     churn: int = 64       # fresh-peer threshold on y >> 56 (64/256 = 25 %)
     seed: int = 1
+    burst: int = 0        # > 0: packet trains of 1 + Geom(1/2) copies, at most `burst`
     _tables: tuple = field(default=None, init=False, repr=False, compare=False)
 
     def tables(self):
@@ -96,6 +104,15 @@ def generate(cfg: TraceConfig, t: int, start: int = 0, count: int | None = None)
     cdf, U = cfg.tables()
     i = np.arange(start, start + count, dtype=np.uint64)
     base = sm64(np.uint64(cfg.seed) ^ (np.uint64(t) << np.uint64(32)))
+    if cfg.burst > 0:  # walk back to the first position of the train
+        src = i.copy()
+        live = np.ones(count, dtype=bool)
+        for _ in range(cfg.burst - 1):
+            cont = (sm64(sm64(base ^ src) ^ np.uint64(0xD1B54A32D192ED03)) >> np.uint64(63)) == 1
+            step = live & cont & (src > 0)
+            src = np.where(step, src - np.uint64(1), src)
+            live = step
+        i = src
     x = sm64(base ^ i)
     u = (x >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
     h = np.searchsorted(cdf, u, side="right").astype(np.uint64)
@@ -118,6 +135,9 @@ def generate(cfg: TraceConfig, t: int, start: int = 0, count: int | None = None)
 CONFIGS = {
     "tiny": TraceConfig("tiny", hosts=64, pairs_per_slice=10_000, U0=4000),
     "caida": TraceConfig("caida", hosts=500_000, pairs_per_slice=5_000_000, U0=1 << 20),
+    # caida with packet trains (SURVEY.md 8 d.3 bursty variant), for the scan modes
+    "caida_bursty": TraceConfig("caida_bursty", hosts=500_000, pairs_per_slice=5_000_000,
+                                U0=1 << 20, burst=16),
     "10G": TraceConfig("10G", hosts=4_000_000, pairs_per_slice=100_000_000, U0=1 << 22),
     "bigwin": TraceConfig("bigwin", hosts=1 << 24, pairs_per_slice=16_666_667, U0=1 << 22),
 }
@@ -138,7 +158,7 @@ def _cuda_lib():
         _cuda.synth_generate.restype = C.c_int
         _cuda.synth_generate.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                          C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint32,
-                                         C.c_uint32, C.c_void_p]
+                                         C.c_uint32, C.c_uint32, C.c_void_p]
     return _cuda
 
 
@@ -160,7 +180,7 @@ class DeviceTrace:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         rc = _cuda_lib().synth_generate(out.data_ptr(), count, self.cfg.seed, t, start,
                                         self.cdf.data_ptr(), self.U.data_ptr(), self.cfg.hosts,
-                                        self.cfg.churn, C.c_void_p(s.cuda_stream))
+                                        self.cfg.churn, self.cfg.burst, C.c_void_p(s.cuda_stream))
         if rc != 0:
             raise RuntimeError(f"synth_generate failed: {rc}")
         return out

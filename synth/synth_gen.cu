@@ -24,10 +24,16 @@ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
 
 __global__ void k_generate(uint2 *__restrict__ out, uint64_t count, uint64_t base, uint64_t start,
                            const double *__restrict__ cdf, const uint32_t *__restrict__ U,
-                           uint32_t H, uint32_t churn) {
+                           uint32_t H, uint32_t churn, uint32_t burst) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < count; q += stride) {
-    const uint64_t x = sm64(base ^ (start + q));
+    uint64_t src = start + q;
+    // bursty variant: back to the first position of the packet train
+    for (uint32_t k = 1; k < burst && src > 0; ++k) {
+      if ((sm64(sm64(base ^ src) ^ 0xD1B54A32D192ED03ull) >> 63) == 0) break;
+      --src;
+    }
+    const uint64_t x = sm64(base ^ src);
     const double u = (double)(x >> 11) * 0x1.0p-53;
     // first index with cdf[h] > u (numpy searchsorted side='right')
     uint32_t lo = 0, hi = H - 1;  // cdf[H-1] = 1.0 > u
@@ -50,7 +56,7 @@ __global__ void k_generate(uint2 *__restrict__ out, uint64_t count, uint64_t bas
 
 extern "C" int synth_generate(void *d_out, uint64_t count, uint64_t seed, uint64_t t,
                               uint64_t start, const void *d_cdf, const void *d_U, uint32_t H,
-                              uint32_t churn, void *stream) {
+                              uint32_t churn, uint32_t burst, void *stream) {
   if (count == 0) return 0;
   if (!d_out || !d_cdf || !d_U || H == 0) return -1;
   // base = sm64(seed ^ (t << 32)), computed on the host exactly as numpy does
@@ -61,6 +67,7 @@ extern "C" int synth_generate(void *d_out, uint64_t count, uint64_t seed, uint64
   uint64_t blocks = (count + 255) / 256;
   if (blocks > 148ull * 16) blocks = 148ull * 16;
   k_generate<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-      (uint2 *)d_out, count, base, start, (const double *)d_cdf, (const uint32_t *)d_U, H, churn);
+      (uint2 *)d_out, count, base, start, (const double *)d_cdf, (const uint32_t *)d_U, H, churn,
+      burst);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

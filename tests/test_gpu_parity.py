@@ -192,6 +192,28 @@ def test_order_split_and_duplicates_give_identical_state():
         assert np.array_equal(a.export_regmax(), b.export_regmax())
 
 
+@pytest.mark.parametrize("layout", ["fast", "packed"])
+@pytest.mark.parametrize("scan_mode", [1, 2, 3, 5, 6])
+def test_bursty_trains_every_scan_mode(layout, scan_mode):
+    """Packet trains (consecutive duplicate pairs: whole warps hitting the
+    same BDR, the case warp aggregation and the block cache target): state
+    and estimates equal the oracle's in every scan mode."""
+    tr = synth.TraceConfig("tiny_bursty", hosts=64, pairs_per_slice=10_000, U0=4000, burst=8)
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(32, 4, 1 << 12, layout=layout, scan_mode=scan_mode, device=DEV)
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    slices = []
+    for t in range(7):
+        pairs = synth.generate(tr, t)
+        slices.append(pairs)
+        pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+    compare_boundary(pool, ref, [], hosts_np, hosts, np.concatenate(slices[-4:]))
+
+
 def test_binned_scan_chunks_and_full_bins():
     """scan_mode 6 (binned): a call larger than one chunk (several bin + apply
     rounds) and a skewed batch whose records overflow their bin (the direct
@@ -239,7 +261,7 @@ def test_host_buffer_path_matches_device_path():
 
 
 def test_synth_cuda_twin_matches_numpy():
-    for name in ("tiny", "caida"):
+    for name in ("tiny", "caida", "caida_bursty"):
         tr = synth.CONFIGS[name]
         dt = synth.DeviceTrace(tr, DEV)
         for t, start, count in ((0, 0, 10_000), (3, 123_457, 40_001)):

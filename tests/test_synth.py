@@ -36,3 +36,19 @@ def test_cardinality_structure():
     win = len(set().union(*[key(x) for x in s]))
     assert one < 10_000  # duplicates within a slice
     assert one < win < 4 * one
+
+
+def test_bursty_packet_trains():
+    """SURVEY.md 8 d.3 bursty variant: trains of 1 + Geom(1/2) copies (capped),
+    the same i.i.d. pairs underneath, and still generatable by ranges."""
+    tr = synth.CONFIGS["caida_bursty"]
+    p = synth.generate(tr, 0, 0, 100_000)
+    same = (p[1:] == p[:-1]).all(axis=1)
+    assert 0.47 < same.mean() < 0.53  # continuation probability 1/2
+    runs = np.diff(np.flatnonzero(np.r_[True, ~same, True]))
+    assert runs.max() <= tr.burst and 1.9 < runs.mean() < 2.1
+    assert np.array_equal(synth.generate(tr, 2, 12_345, 999), synth.generate(tr, 2, 0, 13_344)[12_345:])
+    # every train head is the i.i.d. pair of its position
+    iid = synth.generate(synth.CONFIGS["caida"], 0, 0, 100_000)
+    heads = np.r_[True, ~same]
+    assert np.array_equal(p[heads], iid[heads])
