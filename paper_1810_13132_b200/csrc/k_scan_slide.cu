@@ -183,13 +183,14 @@ k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       record<FAST, ZB, MODE>(v[u].x, v[u].y, p, tickbits, cache);
-      record<FAST, ZB, MODE>(v[u].z, v[u].w, p, tickbits, cache);
+      // a pair repeating its predecessor (packet trains) is the same update
+      if (v[u].z != v[u].x || v[u].w != v[u].y) record<FAST, ZB, MODE>(v[u].z, v[u].w, p, tickbits, cache);
     }
   }
   for (; i < n2; i += stride) {
     const uint4 v = __ldcs(pairs2 + i);
     record<FAST, ZB, MODE>(v.x, v.y, p, tickbits, cache);
-    record<FAST, ZB, MODE>(v.z, v.w, p, tickbits, cache);
+    if (v.z != v.x || v.w != v.y) record<FAST, ZB, MODE>(v.z, v.w, p, tickbits, cache);
   }
   if (tail != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
     record<FAST, ZB, MODE>(tail[0], tail[1], p, tickbits, cache);
