@@ -459,14 +459,21 @@ def run_vbdr(args):
             fn(first + i)
             evs[i][1].record(stream)
         barrier()
-        return float(sum(a.elapsed_time(b) for a, b in evs)), pool.info()["launches"] - l0
+        per_step = [a.elapsed_time(b) for a, b in evs]
+        return float(sum(per_step)), pool.info()["launches"] - l0, per_step
 
-    serial_total, serial_launches = timed_steps(step, args.warmup + args.steps)
+    serial_total, serial_launches, serial_steps = timed_steps(step, args.warmup + args.steps)
     # headline: the pipelined steady state (same work per step)
     if args.pipeline:
-        local_total, launches = timed_steps(step_pipelined, args.warmup + 2 * args.steps)
+        local_total, launches, local_steps = timed_steps(step_pipelined, args.warmup + 2 * args.steps)
     else:
-        local_total, launches = serial_total, serial_launches
+        local_total, launches, local_steps = serial_total, serial_launches, serial_steps
+    # per-step spread (median and min over the measured slices)
+    step_stats = np.array([np.median(local_steps), np.min(local_steps), np.max(local_steps)])
+    if world > 1:
+        t = torch.tensor(step_stats.tolist(), dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_stats = t.cpu().numpy()
     if world > 1:
         t = torch.tensor([local_total, *per_kernel_local.tolist()], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -593,7 +600,10 @@ def run_vbdr(args):
         "metric": "IP pairs scanned per second through whole slices (scan + slide + estimate)",
         "value": round(value, 3), "unit": "Mpairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
-        "ms_per_step_serial": round(serial_ms, 5), "higher_is_better": True,
+        "ms_per_step_serial": round(serial_ms, 5),
+        "step_ms": {"median": round(float(step_stats[0]), 5), "min": round(float(step_stats[1]), 5),
+                    "max": round(float(step_stats[2]), 5)},
+        "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": args.config, "layout": args.layout, **wl,
                    "pairs_per_slice": tr.pairs_per_slice, "hosts": tr.hosts,
