@@ -206,7 +206,7 @@ def oracle_slice_time(tr: synth.TraceConfig, wl: dict, seconds: float, min_slice
     hosts = tr.host_ids()[:hosts_n]
     slices = [synth.generate(tr, t, 0, np_pairs) for t in range(min(4, max(min_slices, 1)))]
     pool.slice(slices[0])  # warm: touches the whole pool once
-    times = []
+    times, phases = [], []
     t_all = time.perf_counter()
     i = 0
     while (time.perf_counter() - t_all < seconds) or len(times) < min_slices:
@@ -214,14 +214,35 @@ def oracle_slice_time(tr: synth.TraceConfig, wl: dict, seconds: float, min_slice
         t0 = time.perf_counter()
         pool.begin_slice()
         pool.scan(pairs)
+        t1 = time.perf_counter()
         pool.end_slice()
-        pool.estimate(pool.readout(), hosts)
-        times.append(time.perf_counter() - t0)
+        M = pool.readout()
+        t2 = time.perf_counter()
+        pool.estimate(M, hosts)
+        t3 = time.perf_counter()
+        times.append(t3 - t0)
+        phases.append((t1 - t0, t2 - t1, t3 - t2))
         i += 1
     sample = (f"oracle serial VBDR, 1 thread, {'full-size' if scale == 1 else f'1/{scale}-scale'} "
               f"{tr.name} slices: {np_pairs} pairs scanned + {n_phys} BDRs closed + {hosts_n} "
               f"hosts estimated per slice, {len(times)} slices")
-    return float(np.mean(times)), np_pairs, len(times), sample
+    ph = np.mean(np.array(phases), axis=0)
+    detail = {"ns_per_pair_scan": round(ph[0] / np_pairs * 1e9, 2),
+              "ns_per_bdr_close": round(ph[1] / n_phys * 1e9, 2),
+              "ns_per_host_estimate": round(ph[2] / hosts_n * 1e9, 2),
+              "cpu_model": cpu_model(), "host_cpus": os.cpu_count()}
+    return float(np.mean(times)), np_pairs, len(times), sample, detail
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
@@ -592,9 +613,9 @@ def run_vbdr(args):
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        sec, npairs, nsl, sample = oracle_slice_time(tr, wl, args.cpu_seconds, 2, 1)
+        sec, npairs, nsl, sample, detail = oracle_slice_time(tr, wl, args.cpu_seconds, 2, 1)
         cpu = {"value": round(npairs / sec / 1e6, 4), "unit": "Mpairs/s", "cores": 1,
-               "kind": "oracle", "sample": sample}
+               "kind": "oracle", "sample": sample, **detail}
 
     line = {
         "metric": "IP pairs scanned per second through whole slices (scan + slide + estimate)",
