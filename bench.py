@@ -594,7 +594,10 @@ def run_vbdr(args):
                      "traffic": traffic.get("estimate"), "hosts": h1 - h0, "gathers": gathers,
                      "peak_source": f"random 1-byte LDG gather ceiling, {tab} table ({CEIL_SRC})"},
     }
-    if plan is not None:
+    staged = plan is not None and wl["n_phys"] <= (1 << 22)  # else a pass-id plan
+    if plan is not None and not staged:
+        kernels["estimate"]["path"] = "pass-id plan (gathers of this pass's registers only)"
+    if staged:
         # The plan path streams, per slice: 4 B of plan entry per gather, the
         # round starts, the register array once per SM (from L2; counted once
         # here as DRAM bytes), 8 B of estimate per host.
@@ -635,7 +638,9 @@ def run_vbdr(args):
                                 if args.pipeline else "serial"),
                    "scan_mode": args.scan_mode, "est_lanes": args.est_lanes,
                    "estimator": args.estimator,
-                   "estimate_path": "plan" if plan is not None else "gather",
+                   "estimate_path": ("gather" if plan is None else
+                                     "plan (shared-memory staged)" if staged else
+                                     "plan (pass ids, multi-pass gather)"),
                    "plan_build_ms": round(plan_build_ms, 2) if plan_build_ms else None,
                    "plan_bytes": plan.nbytes if plan is not None else None,
                    "zbits": info["zbits"], "words_per_bdr": info["words"],

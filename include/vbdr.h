@@ -231,7 +231,11 @@ vbdr_status vbdr_select_above(vbdr_t *h, const double *d_est, uint64_t n, double
  * register per round into its host's shared-memory accumulator.  Same integer
  * sums, same fp64 finish: results are bit-identical to vbdr_estimate.  Needs
  * n_phys in [64, 2^22], n_hosts <= 7 * 512 * SMs (530k on B200) and
- * g * 2^(L-1) (HLL) or g * 255 below 2^32; otherwise VBDR_ERANGE. */
+ * g * 2^(L-1) (HLL) or g * 255 below 2^32.
+ * Larger pools whose gather estimate runs in 2..4 passes (est_pass_log2)
+ * with 64 <= g <= 2048 get a PASS-ID plan instead: a copy of the host list
+ * and the pass of every (host, i) in 2 bits, so each pass hashes and gathers
+ * only its own registers (same sums, bit-identical).  Otherwise VBDR_ERANGE. */
 
 /* SYNC, host only.  Bytes of the caller's plan buffer for n_hosts hosts. */
 vbdr_status vbdr_plan_bytes(const vbdr_t *h, uint64_t n_hosts, uint64_t *bytes);

@@ -195,8 +195,12 @@ constexpr int kPlanSlots = 7;     // hosts per thread (accumulator slots per lan
 constexpr int kPlanEntCap = 8192; // entries per (CTA, block) staged in shared memory
 constexpr int kPlanStride = 20;   // round starts per (CTA, block): 16 warps + total, 16-byte padded
 struct PlanLayout {
+  uint32_t kind;         // 0: shared-memory staged rounds (k_plan.cu); 1: pass ids
   uint32_t ctas, phases, block_log2;
   uint64_t n_hosts;
+  uint32_t *hosts;       // kind 1: a copy of the host list
+  void *pid;             // kind 1: pass ids
+  uint32_t passes;       // kind 1
   uint32_t *range_base;  // [ctas * phases + 1], entries
   uint32_t *starts;      // [ctas * phases * kPlanStride], rounds
   uint32_t *counts;      // [ctas * phases * kPlanThreads] (build scratch: per (warp, bank))
@@ -209,6 +213,15 @@ cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, 
                        uint32_t A0, uint32_t mask, uint32_t *range_size_scratch, cudaStream_t s);
 cudaError_t estimate_plan(const EstParams &e, const PlanLayout &pl, uint64_t n, double *out,
                           unsigned long long *outS, uint32_t *outV, cudaStream_t s);
+
+// Pass-id plan for multi-pass gather estimates (k_estimate.cu): 2 bits per
+// (host, i), 16 bytes per (host, lane), g / 64 lanes per host.
+uint32_t passplan_lanes(uint32_t g);
+cudaError_t passplan_build(const uint32_t *hosts, uint64_t n, uint32_t g, uint32_t A0,
+                           uint32_t mask, uint32_t pass_log2, void *pid, cudaStream_t s);
+cudaError_t estimate_passplan(const EstParams &e, const uint32_t *hosts, uint64_t n,
+                              const void *pid, uint32_t passes, double *out,
+                              unsigned long long *outS, uint32_t *outV, cudaStream_t s);
 
 cudaError_t select_above(const double *est, uint64_t n, double threshold, uint32_t *idx,
                          unsigned long long *count, cudaStream_t s);

@@ -579,12 +579,41 @@ vbdr_status vbdr_select_above(vbdr_t *h, const double *d_est, uint64_t n, double
   return VBDR_OK;
 }
 
+// Pass-id plan (k_estimate.cu) for pools the staged plan cannot take whose
+// gather estimate runs in 2..4 passes: a copy of the host list, then 16 bytes
+// per (host, lane), g / 64 lanes per host.
+struct PassPlanGeom {
+  uint32_t passes, lanes;
+  uint64_t off_hosts, off_pid, bytes;
+};
+
+bool passplan_geom(const vbdr *h, uint64_t n_hosts, PassPlanGeom *g) {
+  const uint64_t z = h->p.n_phys;
+  if (z <= (1ull << 22) || n_hosts == 0) return false;
+  const uint32_t g_regs = h->cfg.m;
+  if (g_regs < 64 || g_regs / 64 > 32) return false;
+  const uint32_t log2z = log2u(z), pl2 = est_params(h).pass_log2;
+  if (pl2 >= log2z || log2z - pl2 > 2) return false;  // 2..4 passes
+  g->passes = 1u << (log2z - pl2);
+  g->lanes = vbdr_launch::passplan_lanes(g_regs);
+  g->off_hosts = 0;
+  g->off_pid = align256(4 * n_hosts);
+  g->bytes = align256(g->off_pid + 16ull * n_hosts * g->lanes);
+  return true;
+}
+
 vbdr_status vbdr_plan_bytes(const vbdr_t *h, uint64_t n_hosts, uint64_t *bytes) {
   if (!h || !bytes) return VBDR_EINVAL;
   PlanGeom g;
+  PassPlanGeom pg;
   *bytes = 0;
-  if (!plan_geom(h, n_hosts, &g)) return VBDR_ERANGE;
-  *bytes = g.bytes;
+  if (plan_geom(h, n_hosts, &g)) {
+    *bytes = g.bytes;
+  } else if (passplan_geom(h, n_hosts, &pg)) {
+    *bytes = pg.bytes;
+  } else {
+    return VBDR_ERANGE;
+  }
   return VBDR_OK;
 }
 
@@ -592,6 +621,30 @@ vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts
                             uint64_t bytes, void *stream) {
   if (!h) return VBDR_EINVAL;
   PlanGeom g;
+  PassPlanGeom pg;
+  if (!plan_geom(h, n_hosts, &g) && passplan_geom(h, n_hosts, &pg)) {
+    if (!d_hosts || !d_plan || (reinterpret_cast<uintptr_t>(d_plan) & 255u))
+      return fail(h, VBDR_EINVAL, "d_hosts and a 256-byte aligned d_plan are required");
+    if (bytes < pg.bytes) return fail(h, VBDR_ENOMEM, "plan buffer too small");
+    if (vbdr_status s = check_async(h, "before plan_build")) return s;
+    cudaStream_t cs = S(stream);
+    uint8_t *b = static_cast<uint8_t *>(d_plan);
+    vbdr_launch::PlanLayout pl{};
+    pl.kind = 1;
+    pl.n_hosts = n_hosts;
+    pl.hosts = reinterpret_cast<uint32_t *>(b + pg.off_hosts);
+    pl.pid = b + pg.off_pid;
+    pl.passes = pg.passes;
+    cudaError_t e = cudaMemcpyAsync(pl.hosts, d_hosts, 4 * n_hosts, cudaMemcpyDeviceToDevice, cs);
+    if (e == cudaSuccess)
+      e = vbdr_launch::passplan_build(d_hosts, n_hosts, h->cfg.m, h->p.A0, h->p.mask,
+                                      est_params(h).pass_log2, pl.pid, cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (e != cudaSuccess) return cuda_fail(h, e, "plan_build");
+    h->info.launches += 1;
+    h->plans[d_plan] = pl;
+    return VBDR_OK;
+  }
   if (!plan_geom(h, n_hosts, &g)) return fail(h, VBDR_ERANGE, "no plan for this pool / host count");
   if (!d_hosts || !d_plan || (reinterpret_cast<uintptr_t>(d_plan) & 255u))
     return fail(h, VBDR_EINVAL, "d_hosts and a 256-byte aligned d_plan are required");
@@ -621,9 +674,18 @@ static vbdr_status estimate_with_plan(vbdr_t *h, const void *d_plan, double *d_o
   auto it = h->plans.find(d_plan);
   if (it == h->plans.end()) return fail(h, VBDR_EINVAL, "unknown plan (build it with this handle)");
   if (vbdr_status s = check_async(h, "before estimate_plan")) return s;
+  const vbdr_launch::PlanLayout &pl = it->second;
+  if (pl.kind == 1) {
+    const cudaError_t e = vbdr_launch::estimate_passplan(
+        est_params(h), pl.hosts, pl.n_hosts, pl.pid, pl.passes, d_out,
+        reinterpret_cast<unsigned long long *>(d_S), d_V, S(stream));
+    if (e != cudaSuccess) return cuda_fail(h, e, "estimate_plan launch");
+    h->info.launches += pl.passes;
+    return VBDR_OK;
+  }
   const cudaError_t e = vbdr_launch::estimate_plan(
-      est_params(h), it->second, it->second.n_hosts, d_out,
-      reinterpret_cast<unsigned long long *>(d_S), d_V, S(stream));
+      est_params(h), pl, pl.n_hosts, d_out, reinterpret_cast<unsigned long long *>(d_S), d_V,
+      S(stream));
   if (e != cudaSuccess) return cuda_fail(h, e, "estimate_plan launch");
   h->info.launches += 1;
   return VBDR_OK;
@@ -655,6 +717,7 @@ vbdr_status vbdr_plan_check(vbdr_t *h, const void *d_plan, void *stream) {
   if (!h) return VBDR_EINVAL;
   auto it = h->plans.find(d_plan);
   if (it == h->plans.end()) return fail(h, VBDR_EINVAL, "unknown plan");
+  if (it->second.kind == 1) return VBDR_OK;  // pass ids: nothing is staged
   unsigned long long err = 0;
   cudaStream_t cs = S(stream);
   cudaError_t e = cudaMemcpyAsync(&err, it->second.error, 8, cudaMemcpyDeviceToHost, cs);

@@ -90,6 +90,14 @@ def run_large(name, m, k, n_phys, n_slices, layout="fast"):
     assert np.array_equal(V.cpu().numpy().astype(np.uint64), Vo)
     assert np.array_equal(S.cpu().numpy().astype(np.float64) * 2.0 ** -L, Z)
     est = pool.estimate(dev_u32(hosts)).cpu().numpy()
+    try:  # the plan the bench uses for this pool (pass ids for multi-pass pools)
+        plan = pool.plan(dev_u32(hosts))
+    except ValueError:
+        plan = None
+    if plan is not None:
+        assert np.array_equal(pool.estimate_plan(plan).cpu().numpy(), est)
+        S2, V2 = pool.host_sums_plan(plan)
+        assert torch.equal(S2, S) and torch.equal(V2, V)
     want = oracle.estimate_M(M, hosts, b, n_phys)
     g, z = m, n_phys
     Es = oracle.alpha(g) * g * g / Z

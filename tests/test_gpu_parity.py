@@ -670,6 +670,32 @@ def test_plan_accumulator_modes_and_ragged_hosts(g, z_log2, n_hosts):
     pool.plan_check(plan)
 
 
+@pytest.mark.parametrize("g,pass_log2", [(64, 21), (128, 22), (256, 21), (2048, 22)])
+def test_pass_id_plan_multipass(g, pass_log2):
+    """Pools beyond the staged plan whose gather estimate runs in 2..4 passes
+    get a pass-id plan: estimates and sums bit-identical to the gather kernel's
+    (duplicate hosts, a ragged host count, g / 64 = 1..32 lanes)."""
+    tr = synth.CONFIGS["tiny"]
+    pool = VBDR(g, 4, 1 << 23, est_pass_log2=pass_log2, device=DEV)
+    rng = np.random.default_rng(g)
+    hosts_np = rng.integers(0, 2**32, 3001, dtype=np.uint64).astype(np.uint32)
+    hosts_np[5::11] = hosts_np[0]
+    hosts_np[:64] = tr.host_ids()  # hosts with traffic
+    hosts = dev_u32(hosts_np)
+    plan = pool.plan(hosts)
+    before = pool.info()["launches"]
+    for t in range(5):
+        pool.scan_slice(dev_u32(synth.generate(tr, t)))
+        pool.slide()
+        a = pool.estimate_plan(plan).cpu().numpy()
+        assert np.array_equal(a, pool.estimate(hosts).cpu().numpy())
+        S1, V1 = pool.host_sums_plan(plan)
+        S2, V2 = pool.host_sums(hosts)
+        assert torch.equal(S1, S2) and torch.equal(V1, V2)
+    assert pool.info()["launches"] > before
+    pool.plan_check(plan)
+
+
 def test_plan_refuses_large_pools():
     pool = VBDR(256, 10, 1 << 23, device=DEV)
     with pytest.raises(ValueError):
