@@ -297,9 +297,10 @@ class VBDR:
     # ---------------------------------------------------- plan-based estimate
     def plan(self, hosts, stream=None):
         """``vbdr_plan_bytes`` + ``vbdr_plan_build``: preprocess a fixed host
-        list (device u32/int32 tensor) for repeated estimates.  Returns an
-        :class:`EstimatePlan`; raises ValueError when the pool or host count has
-        no plan (use :meth:`estimate`)."""
+        list (device u32/int32 tensor) for repeated estimates -- shared-memory
+        staged rounds for pools up to 2^22 BDRs, pass ids for multi-pass pools
+        (include/vbdr.h).  Returns an :class:`EstimatePlan`; raises ValueError
+        when the pool or host count has no plan (use :meth:`estimate`)."""
         import torch
         n = hosts.numel()
         nbytes = C.c_uint64()
