@@ -70,7 +70,8 @@ def parse():
                          "(collectives on the CPU, no GPU-side waiting between ranks)")
     ap.add_argument("--same-device", action="store_true",
                     help="every rank uses cuda:0 (multi-rank logic test on a 1-GPU box)")
-    ap.add_argument("--merge", default="sharded", choices=["stamps", "delta", "sharded", "p2p"],
+    ap.add_argument("--merge", default="sharded",
+                    choices=["stamps", "delta", "sharded", "sparse", "p2p"],
                     help="N>1 slide merge (paper_1810_13132_b200.slide_merged)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--pipeline", action="store_true",
@@ -302,7 +303,8 @@ def run_vbdr(args):
     import torch.distributed as dist
 
     from paper_1810_13132_b200 import (VBDR, PeerMerge, all_gather_shards, make_config,
-                                       merge_stamps, reduce_scatter_max, shard_range)
+                                       merge_stamps, reduce_scatter_max, shard_range,
+                                       slide_merged)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -406,6 +408,10 @@ def run_vbdr(args):
             pool.slide_peers(peer.peer_delta, peer.j0, peer.j1, peer.peer_regmax, peer.peer_acc)
             mark(evs, 3)
             peer._barrier()
+        elif args.merge == "sparse":
+            slide_merged(pool, group, "sparse", shard=shard_buf)
+            mark(evs, 2)
+            mark(evs, 3)
         elif args.merge == "delta":
             pool.stamp_delta(delta_buf)
             dist.all_reduce(delta_buf, op=dist.ReduceOp.MAX, group=group)

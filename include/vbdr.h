@@ -183,6 +183,27 @@ vbdr_status vbdr_stamp_delta(vbdr_t *h, uint8_t *d_delta, void *stream);
 vbdr_status vbdr_slide_delta(vbdr_t *h, const uint8_t *d_delta, uint64_t j0, uint64_t j1,
                              void *stream);
 
+/* Sparse exchange for pools far sparser than a slice (SURVEY 8(e) iii): list
+ * the BDRs this rank's pairs touched in the open slice, per OWNER rank o of
+ * n_owners equal BDR shards [o S, (o + 1) S), S = n_phys / n_owners (a
+ * multiple of 4, <= 2^27), as u32 records ((j - o S) << 5) | rho into
+ * d_records[o * cap .. o * cap + count_o), and count_o into d_counts[o]
+ * (u64[n_owners]; counts are exact even when they exceed cap, in which case
+ * only the first cap records of that owner are written -- call again with a
+ * larger cap).  Record order within an owner is unspecified.  The caller
+ * exchanges the lists (e.g. all-to-all) and every owner folds the records it
+ * received into its delta shard with vbdr_sparse_apply, then closes the slice
+ * with vbdr_slide_delta over its shard.  VBDR_ESTATE on layout packed. */
+vbdr_status vbdr_sparse_extract(vbdr_t *h, uint32_t n_owners, uint32_t *d_records, uint64_t cap,
+                                uint64_t *d_counts, void *stream);
+
+/* d_delta_shard[j] = max(d_delta_shard[j], rho) for every record (j << 5) |
+ * rho of d_records (u32[n_records], any order, any number of ranks); the
+ * caller zeroes the shard first.  A per-byte max, so the result is the
+ * merged nowLBP1 of the shard whatever the record order. */
+vbdr_status vbdr_sparse_apply(vbdr_t *h, const uint32_t *d_records, uint64_t n_records,
+                              uint8_t *d_delta_shard, void *stream);
+
 /* Fused merge + slide over peer memory (the B200 path: no collective kernel).
  * h_peer_delta is a HOST array of n_peers (1..16) device pointers, one per
  * rank, each to that rank's u8[n_phys] delta from vbdr_stamp_delta -- local or

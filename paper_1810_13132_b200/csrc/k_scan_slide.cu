@@ -550,6 +550,59 @@ __global__ void __launch_bounds__(kThreads) k_delta(DevParams p, uint32_t *__res
   }
 }
 
+// ------------------------------------------------------- sparse exchange
+// SURVEY.md 8(e) iii: for pools far sparser than a slice (bigwin: 0.06 pairs
+// per BDR), the ranks exchange only the BDRs their pairs touched: record
+// ((j - j0(o)) << 5) | rho for every BDR j with a stamp from the open tick,
+// listed per owner rank o (BDR shards of `shard` BDRs), then each owner folds
+// the records it receives into its u8 delta shard with a per-byte max.
+__global__ void __launch_bounds__(kThreads)
+k_sparse_extract(DevParams p, uint64_t shard, uint32_t *__restrict__ records, uint64_t cap,
+                 unsigned long long *__restrict__ counts) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t n = p.n_phys;
+  const uint64_t n_round = (n + 31) & ~uint64_t(31);
+  for (uint64_t j = (uint64_t)blockIdx.x * kThreads + threadIdx.x; j < n_round; j += stride) {
+    uint32_t sv = 0u;
+    if (j < n) sv = __ldcs(p.sr + j);
+    const bool hit = j < n && (sv >> 5) == p.tick;
+    const uint32_t owner = hit ? (uint32_t)(j / shard) : 0xFFFFFFFFu;
+    // one counter atomic per (warp, owner): lanes of a warp share owners
+    const uint32_t peers = __match_any_sync(0xffffffffu, owner);
+    const uint32_t leader = __ffs(peers) - 1u;
+    unsigned long long base = 0;
+    if (hit && lane == leader) base = atomicAdd(counts + owner, (unsigned long long)__popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (hit) {
+      const unsigned long long k = base + __popc(peers & ((1u << lane) - 1u));
+      if (k < cap)
+        records[(uint64_t)owner * cap + k] = (uint32_t)((j - (uint64_t)owner * shard) << 5) | (sv & 31u);
+    }
+  }
+}
+
+// delta[r >> 5] = max(delta[r >> 5], r & 31) for every received record (a
+// byte max by compare-and-swap on the containing word; records for the same
+// BDR come from at most one record per rank).
+__global__ void __launch_bounds__(kThreads)
+k_sparse_apply(const uint32_t *__restrict__ records, uint64_t n, uint32_t *__restrict__ delta4) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const uint32_t r = __ldcs(records + i);
+    const uint64_t jl = r >> 5;
+    const uint32_t rho = r & 31u, sh = 8u * (uint32_t)(jl & 3u);
+    uint32_t *w = delta4 + (jl >> 2);
+    uint32_t old = *w;
+    while (((old >> sh) & 0xFFu) < rho) {
+      const uint32_t want = (old & ~(0xFFu << sh)) | (rho << sh);
+      const uint32_t got = atomicCAS(w, old, want);
+      if (got == old) break;
+      old = got;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ init
 // InitDR on every DR, stamps and registers 0.  Accumulator slot
 // 0 describes the empty window (all M = 0) so estimates before the first
@@ -729,6 +782,22 @@ cudaError_t slide_peers(const DevParams &p, const Peers &peers, uint64_t j0, uin
 
 cudaError_t delta(const DevParams &p, uint8_t *out, cudaStream_t s) {
   k_delta<<<grid_for(k_delta, p.n_phys >> 2), kThreads, 0, s>>>(p, reinterpret_cast<uint32_t *>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t sparse_extract(const DevParams &p, uint32_t owners, uint32_t *records, uint64_t cap,
+                           unsigned long long *counts, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(counts, 0, 8ull * owners, s);
+  if (e != cudaSuccess) return e;
+  k_sparse_extract<<<grid_for(k_sparse_extract, p.n_phys), kThreads, 0, s>>>(
+      p, p.n_phys / owners, records, cap, counts);
+  return cudaGetLastError();
+}
+
+cudaError_t sparse_apply(const uint32_t *records, uint64_t n, uint8_t *delta, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_sparse_apply<<<grid_for(k_sparse_apply, n), kThreads, 0, s>>>(
+      records, n, reinterpret_cast<uint32_t *>(delta));
   return cudaGetLastError();
 }
 

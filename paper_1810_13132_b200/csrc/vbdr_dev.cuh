@@ -223,6 +223,12 @@ cudaError_t estimate_passplan(const EstParams &e, const uint32_t *hosts, uint64_
                               const void *pid, uint32_t passes, double *out,
                               unsigned long long *outS, uint32_t *outV, cudaStream_t s);
 
+// Sparse exchange (k_scan_slide.cu): touched BDRs as per-owner records, and
+// their per-byte max into an owner's delta shard.
+cudaError_t sparse_extract(const DevParams &p, uint32_t owners, uint32_t *records, uint64_t cap,
+                           unsigned long long *counts, cudaStream_t s);
+cudaError_t sparse_apply(const uint32_t *records, uint64_t n, uint8_t *delta, cudaStream_t s);
+
 cudaError_t select_above(const double *est, uint64_t n, double threshold, uint32_t *idx,
                          unsigned long long *count, cudaStream_t s);
 

@@ -523,6 +523,38 @@ vbdr_status vbdr_stamp_delta(vbdr_t *h, uint8_t *d_delta, void *stream) {
   return VBDR_OK;
 }
 
+vbdr_status vbdr_sparse_extract(vbdr_t *h, uint32_t n_owners, uint32_t *d_records,
+                                uint64_t cap, uint64_t *d_counts, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (!h->fast) return fail(h, VBDR_ESTATE, "sparse records exist only in layout fast");
+  if (n_owners < 1 || h->p.n_phys % n_owners || (h->p.n_phys / n_owners) % 4)
+    return fail(h, VBDR_EINVAL, "n_owners must divide n_phys into shards of multiples of 4");
+  if (h->p.n_phys / n_owners > (1ull << 27))
+    return fail(h, VBDR_EINVAL, "shards above 2^27 BDRs do not fit a 32-bit record");
+  if (!d_counts || (cap && !d_records))
+    return fail(h, VBDR_EINVAL, "null d_counts / d_records");
+  if (vbdr_status s = check_async(h, "before sparse_extract")) return s;
+  const cudaError_t e = vbdr_launch::sparse_extract(
+      h->p, n_owners, d_records, cap, reinterpret_cast<unsigned long long *>(d_counts), S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "sparse_extract launch");
+  h->info.launches += 1;
+  return VBDR_OK;
+}
+
+vbdr_status vbdr_sparse_apply(vbdr_t *h, const uint32_t *d_records, uint64_t n_records,
+                              uint8_t *d_delta_shard, void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (!h->fast) return fail(h, VBDR_ESTATE, "sparse records exist only in layout fast");
+  if ((n_records && !d_records) || !d_delta_shard ||
+      (reinterpret_cast<uintptr_t>(d_delta_shard) & 3u))
+    return fail(h, VBDR_EINVAL, "need records and a 4-byte aligned delta shard");
+  if (vbdr_status s = check_async(h, "before sparse_apply")) return s;
+  const cudaError_t e = vbdr_launch::sparse_apply(d_records, n_records, d_delta_shard, S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "sparse_apply launch");
+  h->info.launches += n_records ? 1 : 0;
+  return VBDR_OK;
+}
+
 vbdr_status vbdr_slide_delta(vbdr_t *h, const uint8_t *d_delta, uint64_t j0, uint64_t j1,
                              void *stream) {
   if (!h) return VBDR_EINVAL;

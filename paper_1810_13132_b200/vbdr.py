@@ -49,7 +49,7 @@ SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice",
            "vbdr_slide_peers", "vbdr_plan_bytes", "vbdr_plan_build", "vbdr_estimate_plan",
            "vbdr_host_sums_plan", "vbdr_plan_check", "vbdr_plan_release",
            "vbdr_estimate_plan_host", "vbdr_config_check", "vbdr_select_above",
-           "vbdr_last_error", "vbdr_status_string")
+           "vbdr_sparse_extract", "vbdr_sparse_apply", "vbdr_last_error", "vbdr_status_string")
 
 _lib = None
 
@@ -76,6 +76,8 @@ def lib():
             "vbdr_info": [vp, C.POINTER(vbdr_info_t)],
             "vbdr_export_ages": [vp, vp, C.c_int, vp],
             "vbdr_stamp_delta": [vp, vp, vp],
+            "vbdr_sparse_extract": [vp, u32, vp, u64, vp, vp],
+            "vbdr_sparse_apply": [vp, vp, u64, vp, vp],
             "vbdr_debug_set_tick": [vp, u32],
             "vbdr_slide_peers": [vp, vp, u32, u64, u64, vp, vp, vp],
             "vbdr_plan_bytes": [vp, u64, C.POINTER(u64)],
@@ -233,6 +235,32 @@ class VBDR:
         self._check(lib().vbdr_stamp_delta(self._h, C.c_void_p(out.data_ptr()),
                                            _stream_ptr(stream)), "vbdr_stamp_delta")
         return out
+
+    def sparse_extract(self, n_owners: int, cap: int | None = None, stream=None):
+        """``vbdr_sparse_extract``: the BDRs this slice touched, as u32 records
+        per owner shard.  Returns (records int32[n_owners, cap], counts
+        int64[n_owners]); with cap None the exact per-owner counts are taken
+        first (one extra pass over the stamps) and cap is their maximum."""
+        import torch
+        counts = torch.empty(n_owners, dtype=torch.int64, device=self.device)
+        if cap is None:
+            self._check(lib().vbdr_sparse_extract(self._h, n_owners, None, 0,
+                                                  C.c_void_p(counts.data_ptr()),
+                                                  _stream_ptr(stream)), "vbdr_sparse_extract")
+            cap = max(1, int(counts.max()))
+        records = torch.empty((n_owners, cap), dtype=torch.int32, device=self.device)
+        self._check(lib().vbdr_sparse_extract(self._h, n_owners, C.c_void_p(records.data_ptr()),
+                                              cap, C.c_void_p(counts.data_ptr()),
+                                              _stream_ptr(stream)), "vbdr_sparse_extract")
+        if int(counts.max()) > cap:
+            raise RuntimeError("vbdr_sparse_extract: cap too small")
+        return records, counts
+
+    def sparse_apply(self, records, delta_shard, stream=None):
+        """``vbdr_sparse_apply``: per-byte max of received records into a shard."""
+        self._check(lib().vbdr_sparse_apply(self._h, C.c_void_p(records.data_ptr()),
+                                            records.numel(), C.c_void_p(delta_shard.data_ptr()),
+                                            _stream_ptr(stream)), "vbdr_sparse_apply")
 
     def slide_delta(self, delta, j0: int = 0, j1: int | None = None, stream=None):
         """``vbdr_slide_delta``: close the slice from a merged delta over [j0, j1)."""
@@ -460,7 +488,7 @@ def merge_stamps(pool: "VBDR", group=None):
     return merge_stamps_tensor(pool.sr_view(), group)
 
 
-MERGE_MODES = ("stamps", "delta", "sharded", "p2p")
+MERGE_MODES = ("stamps", "delta", "sharded", "sparse", "p2p")
 
 
 def _world(group):
@@ -557,6 +585,9 @@ def slide_merged(pool: "VBDR", group=None, mode: str = "sharded", delta=None, sh
     sharded: reduce-scatter(MAX) of the u8 deltas; each rank slides only its
              1/N of the BDRs, then all-gathers the registers and all-reduces
              the pool sums (bytes and slide time both /N).
+    sparse : as sharded, but the ranks exchange only the BDRs their pairs
+             touched (vbdr_sparse_extract, all-to-all of u32 records,
+             vbdr_sparse_apply): for pools far sparser than a slice.
     With one rank this is vbdr_slide."""
     import torch.distributed as dist
     world, rank = _world(group)
@@ -566,6 +597,9 @@ def slide_merged(pool: "VBDR", group=None, mode: str = "sharded", delta=None, sh
     if mode == "stamps":
         merge_stamps(pool, group)
         pool.slide()
+        return
+    if mode == "sparse":
+        _slide_sparse(pool, group, world, rank, shard)
         return
     delta = pool.stamp_delta(delta)
     if mode == "delta":
@@ -584,3 +618,43 @@ def slide_merged(pool: "VBDR", group=None, mode: str = "sharded", delta=None, sh
     pool.slide_delta(shard, rank * n, (rank + 1) * n)
     all_gather_shards(pool.regmax_view(), group)
     dist.all_reduce(pool.acc_view(), op=dist.ReduceOp.SUM, group=group)
+
+
+def _slide_sparse(pool: "VBDR", group, world: int, rank: int, shard=None):
+    """slide_merged(mode="sparse"): records of touched BDRs, all-to-all by
+    owner shard, per-byte max into the own delta shard, sharded slide."""
+    import torch
+    import torch.distributed as dist
+    n = pool.n_phys // world
+    if n * world != pool.n_phys or n % 4:
+        raise ValueError("sparse merge needs n_phys divisible by 4 * world size")
+    records, counts = pool.sparse_extract(world)
+    recv_counts = torch.empty_like(counts)
+    _all_to_all(recv_counts, counts, None, None, group)
+    send_sizes = counts.tolist()
+    recv_sizes = recv_counts.tolist()
+    send = torch.cat([records[o, :send_sizes[o]] for o in range(world)])
+    recv = torch.empty(sum(recv_sizes), dtype=torch.int32, device=records.device)
+    _all_to_all(recv, send, recv_sizes, send_sizes, group)
+    if shard is None:
+        shard = torch.empty(n, dtype=torch.uint8, device=records.device)
+    shard.zero_()
+    pool.sparse_apply(recv, shard)
+    pool.slide_delta(shard, rank * n, (rank + 1) * n)
+    all_gather_shards(pool.regmax_view(), group)
+    dist.all_reduce(pool.acc_view(), op=dist.ReduceOp.SUM, group=group)
+
+
+def _all_to_all(out, inp, out_sizes, in_sizes, group=None):
+    """all_to_all_single (NCCL on the GPU tensors; through host memory on
+    backends without CUDA all-to-all, e.g. gloo in the tests)."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_to_all_single(out, inp, output_split_sizes=out_sizes,
+                               input_split_sizes=in_sizes, group=group)
+        return out
+    o = out.cpu()
+    dist.all_to_all_single(o, inp.cpu(), output_split_sizes=out_sizes,
+                           input_split_sizes=in_sizes, group=group)
+    out.copy_(o)
+    return out

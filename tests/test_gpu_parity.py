@@ -341,13 +341,16 @@ def test_loopback_multi_rank_merge(n_ranks):
     check_estimates(np.concatenate(parts), ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
 
 
-@pytest.mark.parametrize("mode", ["delta", "sharded"])
+@pytest.mark.parametrize("mode", ["delta", "sharded", "sparse"])
 @pytest.mark.parametrize("n_ranks", [2, 8])
 def test_loopback_delta_merge(mode, n_ranks):
     """The u8-delta merges of slide_merged, with the collectives emulated on one
     GPU: 'delta' (elementwise max of the deltas, every rank slides all BDRs)
     and 'sharded' (rank r slides only its 1/N of the BDRs from the merged
     delta, then the registers are all-gathered and the pool sums all-reduced).
+    'sparse' builds each rank's shard from the touched-BDR records the other
+    ranks extracted for it (vbdr_sparse_extract / vbdr_sparse_apply, the
+    all-to-all emulated) and must equal the merged delta's shard byte for byte.
     Every rank's registers, its shard's DR ages, the pool sums and the
     host-sharded estimates are bit-exact / 1e-9 against the oracle."""
     from paper_1810_13132_b200 import shard_range
@@ -371,8 +374,24 @@ def test_loopback_delta_merge(mode, n_ranks):
             for pool in ranks:
                 pool.slide_delta(merged)
         else:
+            if mode == "sparse":
+                out = [pool.sparse_extract(n_ranks) for pool in ranks]
+                for src, (rec, cnt) in enumerate(out):  # the touched BDRs, exactly
+                    d = deltas[src].cpu().numpy()
+                    for o in range(n_ranks):
+                        got = rec[o, :int(cnt[o])].cpu().numpy().view(np.uint32)
+                        pos = (got >> 5).astype(np.int64)
+                        assert np.array_equal(np.sort(pos), np.flatnonzero(d[o * n:(o + 1) * n]))
+                        assert np.array_equal(d[o * n + pos], (got & 31).astype(np.uint8))
             for r, pool in enumerate(ranks):
-                pool.slide_delta(merged[r * n:(r + 1) * n].clone(), r * n, (r + 1) * n)
+                if mode == "sparse":
+                    shard = torch.zeros(n, dtype=torch.uint8, device=DEV)
+                    for rec, cnt in out:
+                        pool.sparse_apply(rec[r, :int(cnt[r])].contiguous(), shard)
+                    assert torch.equal(shard, merged[r * n:(r + 1) * n])
+                else:
+                    shard = merged[r * n:(r + 1) * n].clone()
+                pool.slide_delta(shard, r * n, (r + 1) * n)
             full = torch.cat([pool.regmax_view()[r * n:(r + 1) * n] for r, pool in enumerate(ranks)])
             acc = sum(pool.acc_view() for pool in ranks)
             for pool in ranks:
