@@ -70,6 +70,9 @@ def parse():
                          "(collectives on the CPU, no GPU-side waiting between ranks)")
     ap.add_argument("--same-device", action="store_true",
                     help="every rank uses cuda:0 (multi-rank logic test on a 1-GPU box)")
+    ap.add_argument("--shard-state", action="store_true",
+                    help="N>1 with --merge sharded/sparse: each rank stores only its "
+                         "shard's DRV (register-sharded state, DRV memory /N)")
     ap.add_argument("--merge", default="sharded",
                     choices=["stamps", "delta", "sharded", "sparse", "p2p"],
                     help="N>1 slide merge (paper_1810_13132_b200.slide_merged)")
@@ -332,9 +335,11 @@ def run_vbdr(args):
     state = None
     if world > 1 and args.merge == "p2p":  # pool state in symmetric memory (peer-writable)
         state = PeerMerge.alloc_state(make_config(wl["m"], wl["k"], wl["n_phys"]), dev)
+    shard_state = args.shard_state and world > 1 and args.merge in ("sharded", "sparse")
     pool = VBDR(wl["m"], wl["k"], wl["n_phys"], layout=args.layout, scan_mode=args.scan_mode,
                 est_lanes=args.est_lanes, est_pass_log2=args.est_pass_log2,
-                estimator=args.estimator, device=dev, state=state)
+                estimator=args.estimator, device=dev, state=state,
+                drv_shards=world if shard_state else 0, drv_shard=rank if shard_state else 0)
     peer = PeerMerge(pool, group) if state is not None else None
     info = pool.info()
     p0, p1 = shard_range(tr.pairs_per_slice, rank, world)
@@ -638,6 +643,7 @@ def run_vbdr(args):
         "config": {"workload": args.config, "layout": args.layout, **wl,
                    "pairs_per_slice": tr.pairs_per_slice, "hosts": tr.hosts,
                    "parallelism": (f"pairs+hosts sharded x{world}, merge={args.merge}"
+                                   + (", register-sharded state" if shard_state else "")
                                    if world > 1 else "single GPU"),
                    "l2": f"flushed before every step ({args.flush_mib} MiB write)",
                    "schedule": ("pipelined: estimate(t) on a 2nd stream overlaps scan(t+1)"

@@ -110,6 +110,17 @@ typedef struct {
      * (vbdr_export_regmax) holds R; the pool sums are sum R (LogLog: sum M)
      * and the zero count. */
     uint32_t estimator;
+    /* drv_shards / drv_shard: register-sharded state (layout
+     * fast only).  With drv_shards = N > 1 the handle stores the packed DRV
+     * of BDRs [r S, (r + 1) S) only (r = drv_shard, S = n_phys / N, a
+     * multiple of 4), so DRV memory is /N; stamps and registers stay
+     * full-size (every rank scans anywhere and estimates from all registers).
+     * Such a handle closes slices only with vbdr_slide_delta /
+     * vbdr_slide_peers over its own shard (vbdr_slide and vbdr_export_ages
+     * return VBDR_ESTATE; vbdr_export_ages_at reads zeros outside the shard).
+     * 0 or 1 = unsharded. */
+    uint32_t drv_shards;
+    uint32_t drv_shard;
 } vbdr_config;
 
 /* Derived sizes and the layout of the state buffer (byte offsets from the

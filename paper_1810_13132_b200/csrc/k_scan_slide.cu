@@ -398,8 +398,9 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
   pdl_wait();
   using S = Swar<ZB>;
   constexpr int WM = WMax<ZB>::value;
-  const uint64_t n4 = p.n_phys >> 2;
   const uint4 *sr4 = reinterpret_cast<const uint4 *>(p.sr);
+  // the DRV holds BDR quads [dq0, dq0 + dn4) (all of them unless register-sharded)
+  const uint64_t dn4 = p.drv_n >> 2, dq0 = p.drv_j0 >> 2;
   uint4 *drv4 = reinterpret_cast<uint4 *>(p.drv);
   uint32_t *reg4 = reinterpret_cast<uint32_t *>(p.regmax);
   unsigned long long s_acc = 0;
@@ -426,7 +427,7 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
     uint4 x[WM];
 #pragma unroll
     for (int w = 0; w < WM; ++w)
-      if (w < (int)p.W) x[w] = drv4[(uint64_t)w * n4 + q];
+      if (w < (int)p.W) x[w] = drv4[(uint64_t)w * dn4 + (q - dq0)];
     uint32_t best[4] = {0u, 0u, 0u, 0u};
     uint32_t run[4] = {0u, 0u, 0u, 0u};  // PCSA: active ranks from the bottom of word w up
 #pragma unroll
@@ -451,7 +452,7 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
       // warp (typical for the high-rank words) skip the SWAR work.
       if (__all_sync(__activemask(), sat)) {
 #if VBDR_SLIDE_SKIP == 2
-        drv4[(uint64_t)w * n4 + q] = x[w];  // unchanged, stored anyway
+        drv4[(uint64_t)w * dn4 + (q - dq0)] = x[w];  // unchanged, stored anyway
 #endif
         if constexpr (PCSA) {
 #pragma unroll
@@ -476,7 +477,7 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
           run[c] = inact ? (uint32_t)(__ffs(inact) - 1) / (uint32_t)ZB : (uint32_t)S::F + run[c];
         }
       }
-      drv4[(uint64_t)w * n4 + q] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
+      drv4[(uint64_t)w * dn4 + (q - dq0)] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
     }
     if constexpr (PCSA) {
 #pragma unroll
@@ -613,8 +614,11 @@ __global__ void __launch_bounds__(kThreads) k_init(DevParams p, bool fast) {
   const uint64_t n4 = p.n_phys >> 2;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   uint4 *drv4 = reinterpret_cast<uint4 *>(p.drv);
+  const uint64_t dn4 = p.drv_n >> 2, dq0 = p.drv_j0 >> 2;
   for (uint64_t q = (uint64_t)blockIdx.x * kThreads + threadIdx.x; q < n4; q += stride) {
-    for (uint32_t w = 0; w < p.W; ++w) drv4[(uint64_t)w * n4 + q] = make_uint4(S::INIT, S::INIT, S::INIT, S::INIT);
+    if (q >= dq0 && q < dq0 + dn4)
+      for (uint32_t w = 0; w < p.W; ++w)
+        drv4[(uint64_t)w * dn4 + (q - dq0)] = make_uint4(S::INIT, S::INIT, S::INIT, S::INIT);
     if (fast) reinterpret_cast<uint4 *>(p.sr)[q] = make_uint4(0u, 0u, 0u, 0u);
     reinterpret_cast<uint32_t *>(p.regmax)[q] = 0u;
   }
@@ -634,7 +638,9 @@ k_gather_words(DevParams p, const uint64_t *__restrict__ idx, uint64_t n, uint32
   for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
     const uint64_t j = idx[i];
     for (uint32_t w = 0; w < p.W; ++w)
-      out[i * p.W + w] = j < p.n_phys ? p.drv[(uint64_t)w * p.n_phys + j] : 0u;
+      out[i * p.W + w] = (j >= p.drv_j0 && j < p.drv_j0 + p.drv_n)
+                             ? p.drv[(uint64_t)w * p.drv_n + (j - p.drv_j0)]
+                             : 0u;  // outside the (shard of the) pool
   }
 }
 

@@ -12,10 +12,11 @@ namespace vbdr_dev {
 // Parameters every kernel receives by value.
 struct DevParams {
   uint32_t *sr;              // u32[n_phys] stamp words (layout F)
-  uint32_t *drv;             // u32[W][n_phys] packed DRV, plane-major
+  uint32_t *drv;             // u32[W][drv_n] packed DRV of BDRs [drv_j0, drv_j0 + drv_n), plane-major
   uint8_t *regmax;           // u8[n_phys] register values M[j]
   unsigned long long *acc;   // u64[4]: (S_tot, V_tot) per tick parity
   uint64_t n_phys;
+  uint64_t drv_j0, drv_n;    // the DRV shard (0, n_phys unless register-sharded)
   uint32_t mask;             // n_phys - 1 (n_phys <= 2^32)
   uint32_t b, L, k, zb, F, W;
   uint32_t A0, A1;

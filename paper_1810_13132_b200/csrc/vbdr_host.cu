@@ -113,6 +113,14 @@ std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *p
     return "est_lanes must be 0 or a power of two <= 32";
   if (n.est_pass_log2 > 32) return "est_pass_log2 must be 0..32";
   if (n.estimator > 2) return "estimator must be 0 (HLL), 1 (LogLog) or 2 (PCSA)";
+  if (n.drv_shards > 1) {
+    if (n.layout != VBDR_LAYOUT_FAST) return "drv_shards needs layout fast";
+    if (n.drv_shard >= n.drv_shards) return "drv_shard must be < drv_shards";
+    if (n.n_phys % n.drv_shards || (n.n_phys / n.drv_shards) % 4)
+      return "drv_shards must split n_phys into shards of multiples of 4";
+  } else if (n.drv_shard != 0) {
+    return "drv_shard needs drv_shards > 1";
+  }
   if (n.estimator == 2 && n.layout != VBDR_LAYOUT_PACKED)
     return "PCSA needs layout packed (every rank recorded: the sliding bitmap)";
   if (n.m < 2 || !is_pow2(n.m)) return "m must be a power of two >= 2";
@@ -147,7 +155,8 @@ std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *p
   pl->off_sr = off;
   if (!packed) off = align256(off + 4ull * n.n_phys);
   pl->off_drv = off;
-  off = align256(off + 4ull * W * n.n_phys);
+  const uint64_t drv_n = n.drv_shards > 1 ? n.n_phys / n.drv_shards : n.n_phys;
+  off = align256(off + 4ull * W * drv_n);
   pl->off_regmax = off;
   off = align256(off + n.n_phys);
   if (effective_scan_mode(n) == 6) {
@@ -410,6 +419,8 @@ vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, v
   p.drv = reinterpret_cast<uint32_t *>(base + pl.off_drv);
   p.regmax = base + pl.off_regmax;
   p.n_phys = h->cfg.n_phys;
+  p.drv_n = h->cfg.drv_shards > 1 ? h->cfg.n_phys / h->cfg.drv_shards : h->cfg.n_phys;
+  p.drv_j0 = h->cfg.drv_shards > 1 ? p.drv_n * h->cfg.drv_shard : 0;
   p.mask = (uint32_t)(h->cfg.n_phys - 1);
   p.b = pl.b;
   p.L = pl.L;
@@ -493,8 +504,15 @@ vbdr_status vbdr_scan_slice(vbdr_t *h, const uint32_t *d_pairs, uint64_t n_pairs
   return VBDR_OK;
 }
 
+// A register-sharded handle only holds the DRV of [drv_j0, drv_j0 + drv_n).
+bool drv_covers(const vbdr *h, uint64_t j0, uint64_t j1) {
+  return j0 >= h->p.drv_j0 && j1 <= h->p.drv_j0 + h->p.drv_n;
+}
+
 vbdr_status vbdr_slide(vbdr_t *h, void *stream) {
   if (!h) return VBDR_EINVAL;
+  if (h->p.drv_n != h->p.n_phys)
+    return fail(h, VBDR_ESTATE, "a register-sharded handle closes slices with slide_delta");
   if (vbdr_status s = check_async(h, "before slide")) return s;
   const cudaError_t e = vbdr_launch::slide(h->p, h->fast, S(stream));
   if (e != cudaSuccess) return cuda_fail(h, e, "slide launch");
@@ -562,6 +580,8 @@ vbdr_status vbdr_slide_delta(vbdr_t *h, const uint8_t *d_delta, uint64_t j0, uin
   if (!d_delta || (reinterpret_cast<uintptr_t>(d_delta) & 3u) || j0 >= j1 || j1 > h->p.n_phys ||
       (j0 & 3u) || (j1 & 3u))
     return fail(h, VBDR_EINVAL, "need a 4-byte aligned delta and 0 <= j0 < j1 <= n_phys, both multiples of 4");
+  if (!drv_covers(h, j0, j1))
+    return fail(h, VBDR_EINVAL, "[j0, j1) outside this handle's DRV shard");
   if (vbdr_status s = check_async(h, "before slide_delta")) return s;
   const cudaError_t e = vbdr_launch::slide_delta(h->p, d_delta, j0, j1, S(stream));
   if (e != cudaSuccess) return cuda_fail(h, e, "slide_delta launch");
@@ -576,6 +596,8 @@ vbdr_status vbdr_slide_peers(vbdr_t *h, const uint8_t *const *h_peer_delta, uint
   if (!h_peer_delta || n_peers < 1 || n_peers > (uint32_t)vbdr_launch::kMaxPeers || j0 >= j1 ||
       j1 > h->p.n_phys || (j0 & 3u) || (j1 & 3u))
     return fail(h, VBDR_EINVAL, "need 1..16 peer deltas and 0 <= j0 < j1 <= n_phys, multiples of 4");
+  if (!drv_covers(h, j0, j1))
+    return fail(h, VBDR_EINVAL, "[j0, j1) outside this handle's DRV shard");
   vbdr_launch::Peers pe{};
   pe.n = n_peers;
   for (uint32_t r = 0; r < n_peers; ++r) {
@@ -868,6 +890,8 @@ vbdr_status vbdr_estimate_host(vbdr_t *h, const uint32_t *h_hosts, uint64_t n_ho
 
 vbdr_status vbdr_export_ages(vbdr_t *h, uint16_t *h_ages, int mode, void *stream) {
   if (!h || !h_ages || (mode != 0 && mode != 1)) return VBDR_EINVAL;
+  if (h->p.drv_n != h->p.n_phys)
+    return fail(h, VBDR_ESTATE, "a register-sharded handle exports ages with export_ages_at");
   const uint64_t n = h->p.n_phys;
   const uint32_t W = h->p.W;
   std::vector<uint32_t> words;

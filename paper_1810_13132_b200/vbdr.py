@@ -30,7 +30,7 @@ class vbdr_config(C.Structure):
                 ("seed_a0", C.c_uint32), ("seed_a1", C.c_uint32), ("zbits", C.c_uint32),
                 ("rank_cap", C.c_uint32), ("layout", C.c_uint32), ("scan_mode", C.c_uint32),
                 ("est_lanes", C.c_uint32), ("est_pass_log2", C.c_uint32),
-                ("estimator", C.c_uint32)]
+                ("estimator", C.c_uint32), ("drv_shards", C.c_uint32), ("drv_shard", C.c_uint32)]
 
 
 class vbdr_info_t(C.Structure):
@@ -111,11 +111,12 @@ def make_config(m: int, k: int, n_phys: int, seed_a0: int = 0x5EED0001,
                 seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
                 layout: str | int = "fast", scan_mode: int = 0,
                 est_lanes: int = 0, est_pass_log2: int = 0,
-                estimator: str | int = "hll") -> vbdr_config:
+                estimator: str | int = "hll", drv_shards: int = 0,
+                drv_shard: int = 0) -> vbdr_config:
     lay = LAYOUTS[layout] if isinstance(layout, str) else int(layout)
     est = ESTIMATORS[estimator] if isinstance(estimator, str) else int(estimator)
     return vbdr_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, lay, scan_mode, est_lanes,
-                       est_pass_log2, est)
+                       est_pass_log2, est, drv_shards, drv_shard)
 
 
 def state_bytes(cfg: vbdr_config) -> int:
@@ -141,13 +142,13 @@ class VBDR:
                  seed_a1: int = 0x5EED0002, zbits: int = 0, rank_cap: int = 0,
                  layout: str = "fast", scan_mode: int = 0, est_lanes: int = 0,
                  est_pass_log2: int = 0, estimator: str = "hll", device=None, stream=None,
-                 state=None):
+                 state=None, drv_shards: int = 0, drv_shard: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("VBDR needs a CUDA device (no CPU fallback)")
         self.device = torch.device(device if device is not None else "cuda")
         self.cfg = make_config(m, k, n_phys, seed_a0, seed_a1, zbits, rank_cap, layout, scan_mode,
-                               est_lanes, est_pass_log2, estimator)
+                               est_lanes, est_pass_log2, estimator, drv_shards, drv_shard)
         self.estimator = estimator
         nbytes = state_bytes(self.cfg)
         with torch.cuda.device(self.device):

@@ -25,7 +25,13 @@ def main(mode: str):
     torch.cuda.set_device(dev)
     tr = synth.CONFIGS["tiny"]
     cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
-    pool = VBDR(32, 4, 1 << 12, device=dev)
+    # "sharded-state": the sharded merge on register-sharded handles (each
+    # rank stores only its shard's DRV)
+    sharded_state = mode == "sharded-state"
+    if sharded_state:
+        mode = "sharded"
+    pool = VBDR(32, 4, 1 << 12, device=dev, drv_shards=world if sharded_state else 0,
+                drv_shard=rank if sharded_state else 0)
     ref = oracle.Pool(cfg, "serial") if rank == 0 else None
     ok = True
     for t in range(7):
@@ -55,7 +61,8 @@ def main(mode: str):
         got = np.concatenate(parts)
         want = ref.estimate(ref.readout(), hosts)
         ok &= bool(np.all(np.abs(got - want) <= 1e-9 * np.maximum(np.abs(want), 1.0)))
-        print(f"mode={mode} world={world} parity={'ok' if ok else 'FAILED'}", flush=True)
+        print(f"mode={mode}{' (sharded state)' if sharded_state else ''} world={world} "
+              f"parity={'ok' if ok else 'FAILED'}", flush=True)
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)

@@ -30,7 +30,7 @@ def _torchrun(n, *args):
     return subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
 
 
-@pytest.mark.parametrize("mode", ["stamps", "delta", "sharded", "sparse"])
+@pytest.mark.parametrize("mode", ["stamps", "delta", "sharded", "sparse", "sharded-state"])
 @pytest.mark.parametrize("world", [2, 4])
 def test_slide_merged_multi_rank(mode, world):
     r = _torchrun(world, os.path.join("tests", "dist_worker.py"), mode)

@@ -214,6 +214,27 @@ def test_bursty_trains_every_scan_mode(layout, scan_mode):
     compare_boundary(pool, ref, [], hosts_np, hosts, np.concatenate(slices[-4:]))
 
 
+def test_register_sharded_state_rules():
+    """drv_shards: the DRV of one shard only; closing or exporting the whole
+    pool is refused, slide_delta outside the shard is refused."""
+    with pytest.raises(ValueError):
+        VBDR(32, 4, 1 << 12, device=DEV, layout="packed", drv_shards=2)
+    with pytest.raises(ValueError):
+        VBDR(32, 4, 1 << 12, device=DEV, drv_shards=2, drv_shard=2)
+    pool = VBDR(32, 4, 1 << 12, device=DEV, drv_shards=4, drv_shard=1)
+    pool.scan_slice(dev_u32(synth.generate(synth.CONFIGS["tiny"], 0)))
+    with pytest.raises(RuntimeError, match="ESTATE"):
+        pool.slide()
+    with pytest.raises(RuntimeError, match="ESTATE"):
+        pool.export_ages()
+    delta = pool.stamp_delta()
+    with pytest.raises(RuntimeError, match="EINVAL"):
+        pool.slide_delta(delta[:1024].clone(), 0, 1024)
+    pool.slide_delta(delta[1024:2048].clone(), 1024, 2048)
+    ages = pool.export_ages_at(np.array([0, 1024, 2047, 2048], dtype=np.uint64))
+    assert (ages[0] == 0).all() and (ages[3] == 0).all()  # outside the shard
+
+
 def test_binned_scan_chunks_and_full_bins():
     """scan_mode 6 (binned): a call larger than one chunk (several bin + apply
     rounds) and a skewed batch whose records overflow their bin (the direct
@@ -341,7 +362,7 @@ def test_loopback_multi_rank_merge(n_ranks):
     check_estimates(np.concatenate(parts), ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
 
 
-@pytest.mark.parametrize("mode", ["delta", "sharded", "sparse"])
+@pytest.mark.parametrize("mode", ["delta", "sharded", "sparse", "sharded-state"])
 @pytest.mark.parametrize("n_ranks", [2, 8])
 def test_loopback_delta_merge(mode, n_ranks):
     """The u8-delta merges of slide_merged, with the collectives emulated on one
@@ -351,13 +372,21 @@ def test_loopback_delta_merge(mode, n_ranks):
     'sparse' builds each rank's shard from the touched-BDR records the other
     ranks extracted for it (vbdr_sparse_extract / vbdr_sparse_apply, the
     all-to-all emulated) and must equal the merged delta's shard byte for byte.
+    'sharded-state' is 'sharded' with register-sharded handles (drv_shards =
+    N: each rank stores only its shard's DRV).
     Every rank's registers, its shard's DR ages, the pool sums and the
     host-sharded estimates are bit-exact / 1e-9 against the oracle."""
     from paper_1810_13132_b200 import shard_range
     tr = synth.CONFIGS["tiny"]
     cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
     ref = oracle.Pool(cfg, "serial")
-    ranks = [VBDR(32, 4, 1 << 12, device=DEV) for _ in range(n_ranks)]
+    if mode == "sharded-state":
+        ranks = [VBDR(32, 4, 1 << 12, device=DEV, drv_shards=n_ranks, drv_shard=r)
+                 for r in range(n_ranks)]
+        full = VBDR(32, 4, 1 << 12, device=DEV)
+        assert ranks[0].info()["state_bytes"] < full.info()["state_bytes"]
+    else:
+        ranks = [VBDR(32, 4, 1 << 12, device=DEV) for _ in range(n_ranks)]
     n = cfg.z // n_ranks
     hosts_np = tr.host_ids()
     for t in range(7):
@@ -403,7 +432,11 @@ def test_loopback_delta_merge(mode, n_ranks):
             assert np.array_equal(pool.export_regmax(), M)
             assert pool.export_pool_sums() == oracle_pool_sums(M, cfg.L)
             j0, j1 = (0, cfg.z) if mode == "delta" else (r * n, (r + 1) * n)
-            assert np.array_equal(pool.export_ages()[j0:j1], drv[j0:j1])
+            if mode == "sharded-state":  # only the shard's DRV exists
+                idx = np.arange(j0, j1, dtype=np.uint64)
+                assert np.array_equal(pool.export_ages_at(idx), drv[j0:j1])
+            else:
+                assert np.array_equal(pool.export_ages()[j0:j1], drv[j0:j1])
     parts = []
     for r, pool in enumerate(ranks):
         h0, h1 = shard_range(len(hosts_np), r, n_ranks)
