@@ -214,6 +214,22 @@ def test_bursty_trains_every_scan_mode(layout, scan_mode):
     compare_boundary(pool, ref, [], hosts_np, hosts, np.concatenate(slices[-4:]))
 
 
+def test_sparse_extract_counts_and_cap():
+    """vbdr_sparse_extract: exact per-owner counts even when the cap is too
+    small (the binding then raises), and no records at all for an empty slice."""
+    pool = VBDR(32, 4, 1 << 12, device=DEV)
+    rec, cnt = pool.sparse_extract(4)
+    assert int(cnt.sum()) == 0
+    pairs = synth.generate(synth.CONFIGS["tiny"], 0)
+    pool.scan_slice(dev_u32(pairs))
+    rec, cnt = pool.sparse_extract(4)
+    assert int(cnt.sum()) == int((pool.stamp_delta() > 0).sum())
+    with pytest.raises(RuntimeError, match="cap"):
+        pool.sparse_extract(4, cap=int(cnt.max()) - 1)
+    with pytest.raises(RuntimeError, match="EINVAL"):
+        pool.sparse_extract(3)  # 4096 BDRs do not split in 3
+
+
 def test_register_sharded_state_rules():
     """drv_shards: the DRV of one shard only; closing or exporting the whole
     pool is refused, slide_delta outside the shard is refused."""
