@@ -634,6 +634,12 @@ def test_estimator_variants_caida(layout, estimator):
     est = pool.estimate(dev_u32(sample)).cpu().numpy()
     want = oracle.estimate_variant(V, sample, cfg.b, cfg.z, estimator)
     check_estimates(est, want, variant_floor(V, sample, cfg.b, cfg.z, estimator))
+    # the bench's plan path for all 500k hosts: bit-identical to the gather
+    hosts = dev_u32(hosts_np)
+    plan = pool.plan(hosts)
+    assert np.array_equal(pool.estimate_plan(plan).cpu().numpy(),
+                          pool.estimate(hosts).cpu().numpy())
+    pool.plan_check(plan)
 
 
 @pytest.mark.parametrize("layout", ["fast", "packed"])
