@@ -77,10 +77,11 @@ def parse():
                     choices=["stamps", "delta", "sharded", "sparse", "p2p"],
                     help="N>1 slide merge (paper_1810_13132_b200.slide_merged)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--pipeline", action="store_true",
-                    help="headline from pipelined steps: the estimate of slice t overlaps the "
-                         "scan of slice t+1 on a second stream (profiles/r01_pipeline.txt: "
-                         "+3 %% at caida, -20 %% at 10G with scan mode 5; default off)")
+    ap.add_argument("--pipeline", default="auto", choices=["auto", "on", "off"],
+                    help="headline from software-pipelined steps: the estimate of slice t "
+                         "overlaps the scan and slide of slice t+1 on a second stream "
+                         "(profiles/r01_pipeline.txt).  auto = on with the shared-memory plan "
+                         "estimate (+9 %% at caida), off with the gather estimate (-24 %% at 10G)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--flush-mib", type=int, default=512)
@@ -446,19 +447,22 @@ def run_vbdr(args):
     ev_closed, ev_est = torch.cuda.Event(), torch.cuda.Event()
 
     def step_pipelined(i):
-        """Steady-state software pipeline: the estimate of the slice closed
-        last (t) runs on a second stream while the scan of slice t+1 runs on
-        the main one; the slide of t+1 then waits for that estimate (it
-        rewrites the registers the estimate reads).  Same work per step as
-        step(): one scan, one slide, one estimate."""
+        """Software-pipelined step: the estimate of the slice closed last (t)
+        runs on a second stream while the scan AND the slide of slice t+1 run
+        on the main one.  The two register buffers alternate with the tick and
+        the pool sums have four slots, so the slide of t+1 writes nothing the
+        estimate of t reads.  The step ends when both streams are done (the
+        main stream joins the estimate), so all of its work is inside the
+        step's events and none overlaps the L2 flush between steps.  Same
+        work per step as step(): one scan, one slide, one estimate."""
         x = inputs[i % n_inputs]
         ev_closed.record(stream)
         stream_b.wait_event(ev_closed)
         estimate(est_out, stream_b)
         ev_est.record(stream_b)
         pool.scan_slice(x)
-        stream.wait_event(ev_est)
         close_slice()
+        stream.wait_event(ev_est)
 
     # warm-up
     for i in range(args.warmup):
@@ -496,7 +500,9 @@ def run_vbdr(args):
 
     serial_total, serial_launches, serial_steps = timed_steps(step, args.warmup + args.steps)
     # headline: the pipelined steady state (same work per step)
-    if args.pipeline:
+    staged_plan = plan is not None and wl["n_phys"] <= (1 << 22)
+    pipelined = args.pipeline == "on" or (args.pipeline == "auto" and staged_plan)
+    if pipelined:
         local_total, launches, local_steps = timed_steps(step_pipelined, args.warmup + 2 * args.steps)
     else:
         local_total, launches, local_steps = serial_total, serial_launches, serial_steps
@@ -646,8 +652,9 @@ def run_vbdr(args):
                                    + (", register-sharded state" if shard_state else "")
                                    if world > 1 else "single GPU"),
                    "l2": f"flushed before every step ({args.flush_mib} MiB write)",
-                   "schedule": ("pipelined: estimate(t) on a 2nd stream overlaps scan(t+1)"
-                                if args.pipeline else "serial"),
+                   "schedule": ("pipelined: estimate(t) on a 2nd stream overlaps scan(t+1) "
+                                "and slide(t+1)"
+                                if pipelined else "serial"),
                    "scan_mode": args.scan_mode, "est_lanes": args.est_lanes,
                    "estimator": args.estimator,
                    "estimate_path": ("gather" if plan is None else

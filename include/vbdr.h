@@ -134,12 +134,14 @@ typedef struct {
     uint32_t tick;         /* T = t + 1 of the open slice t                   */
     uint64_t n_phys;
     uint64_t slices_closed;/* number of vbdr_slide calls so far               */
-    uint64_t off_acc;      /* u64[4]: (S_tot, V_tot) for tick parity 0 and 1  */
+    uint64_t off_acc;      /* u64[8]: (S_tot, V_tot) for tick mod 4 = 0..3    */
     uint64_t off_sr;       /* u32[n_phys] stamp words (LAYOUT_FAST only)      */
     uint64_t off_drv;      /* u32[W][n_phys] packed DRV, plane-major          */
-    uint64_t off_regmax;   /* u8[n_phys] register values M[j] (Alg.2)         */
+    uint64_t off_regmax;   /* u8[n_phys] register values M[j] (Alg.2) of the
+                            * closed tick (two buffers alternate by tick parity) */
     uint64_t state_bytes;  /* total bytes the state buffer needs              */
     uint64_t launches;     /* kernels launched by this handle so far          */
+    uint64_t off_regmax_next; /* the register buffer the next slide writes     */
 } vbdr_info_t;
 
 /* SYNC.  Bytes of device memory the caller must provide for this config. */
@@ -188,7 +190,7 @@ vbdr_status vbdr_stamp_delta(vbdr_t *h, uint8_t *d_delta, void *stream);
  * BDR range [j0, j1) only (multiples of 4; d_delta[j - j0] is BDR j's rank).
  * With [0, n_phys) every rank slides its full replica; with a shard per rank
  * the ranks then all-gather regmax (vbdr_info off_regmax) and all-reduce (SUM)
- * the pool sums of the closed tick (the two u64 at off_acc + 16 * (T & 1),
+ * the pool sums of the closed tick (the two u64 at off_acc + 16 * (T mod 4),
  * T = the closed tick) before estimating.  DRs outside [j0, j1) are not aged
  * and must not be used afterwards.  Closes the slice like vbdr_slide. */
 vbdr_status vbdr_slide_delta(vbdr_t *h, const uint8_t *d_delta, uint64_t j0, uint64_t j1,

@@ -527,9 +527,9 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
       atomicAdd(p.acc + 2 * slot, st);
       atomicAdd(p.acc + 2 * slot + 1, vt);
     }
-    if (blockIdx.x == 0) {  // the other parity's slot is next slide's accumulator
-      p.acc[2 * (slot ^ 1u)] = 0ull;
-      p.acc[2 * (slot ^ 1u) + 1] = 0ull;
+    if (blockIdx.x == 0) {  // the next tick's slot is the next slide's accumulator
+      p.acc[2 * ((slot + 1u) & 3u)] = 0ull;
+      p.acc[2 * ((slot + 1u) & 3u) + 1] = 0ull;
     }
   }
 }
@@ -605,9 +605,10 @@ k_sparse_apply(const uint32_t *__restrict__ records, uint64_t n, uint32_t *__res
 }
 
 // ------------------------------------------------------------------ init
-// InitDR on every DR, stamps and registers 0.  Accumulator slot
-// 0 describes the empty window (all M = 0) so estimates before the first
-// slide are 0; slot 1 is the first slide's accumulator.
+// InitDR on every DR, stamps and registers 0 (the first
+// register buffer; the host clears the second).  Accumulator slot 0 describes
+// the empty window (all M = 0) so estimates before the first slide are 0;
+// slot 1 is the first slide's accumulator.
 template <int ZB>
 __global__ void __launch_bounds__(kThreads) k_init(DevParams p, bool fast) {
   using S = Swar<ZB>;
@@ -625,8 +626,7 @@ __global__ void __launch_bounds__(kThreads) k_init(DevParams p, bool fast) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.acc[0] = p.est == 0u ? (unsigned long long)p.n_phys << p.L : 0ull;
     p.acc[1] = p.n_phys;
-    p.acc[2] = 0ull;
-    p.acc[3] = 0ull;
+    for (int i = 2; i < 8; ++i) p.acc[i] = 0ull;
   }
 }
 
@@ -706,7 +706,7 @@ struct SlideFn {
     // (2^zb - k) at every even field's LSB (Swar::active)
     uint32_t addk = 0;
     for (uint32_t f = 0; f < Swar<ZB>::F; f += 2) addk |= ((1u << ZB) - p.k) << (ZB * f);
-    const uint32_t slot = p.tick & 1u;
+    const uint32_t slot = p.tick & 3u;  // four slots: the estimate of tick T-1 may still read its own
     const uint64_t work = q1 - q0;
     const vbdr_launch::Peers none{};
     if (fast && peers)

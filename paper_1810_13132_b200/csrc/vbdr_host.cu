@@ -30,6 +30,10 @@ struct vbdr {
   std::map<const void *, vbdr_launch::PlanLayout> plans;  // built plans by device address
   cudaEvent_t ev_hosts_in = nullptr;    // host ids copied (copy stream)
   cudaEvent_t ev_hosts_free = nullptr;  // last estimate that read the host stage
+  // two register buffers: the slide of tick T writes buffer T & 1, so the
+  // estimate of tick T - 1 may run concurrently with the next slide
+  uint8_t *regmax_base = nullptr;
+  uint64_t regmax_stride = 0;
 };
 
 namespace vbdr_dev {
@@ -82,7 +86,7 @@ double alpha_of(uint64_t s) {
 
 struct StateLayout {
   uint32_t b, L, zb, F, W;
-  uint64_t off_acc, off_sr, off_drv, off_regmax, bytes;
+  uint64_t off_acc, off_sr, off_drv, off_regmax, regmax_stride, bytes;
   // binned scan (scan_mode 6): bins + cursors, 0 bytes otherwise
   uint32_t bkt_log2 = 0, bcap = 0;
   uint64_t bchunk = 0, off_bins = 0, off_bcursor = 0;
@@ -151,14 +155,15 @@ std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *p
   const uint32_t W = (L + F - 1) / F;
   uint64_t off = 0;
   pl->off_acc = off;
-  off = align256(off + 4 * sizeof(uint64_t));
+  off = align256(off + 8 * sizeof(uint64_t));  // (S_tot, V_tot) for tick mod 4
   pl->off_sr = off;
   if (!packed) off = align256(off + 4ull * n.n_phys);
   pl->off_drv = off;
   const uint64_t drv_n = n.drv_shards > 1 ? n.n_phys / n.drv_shards : n.n_phys;
   off = align256(off + 4ull * W * drv_n);
-  pl->off_regmax = off;
-  off = align256(off + n.n_phys);
+  pl->off_regmax = off;  // two register buffers: the slide of tick T writes buffer T & 1
+  pl->regmax_stride = align256(n.n_phys);
+  off = align256(off + 2 * pl->regmax_stride);
   if (effective_scan_mode(n) == 6) {
     // buckets of 2^14 BDRs (64 KB of ranks in shared memory); chunks of up to
     // 2 n_phys pairs (<= 2^27); bins sized for the mean load + 12.5 % + 512
@@ -218,11 +223,15 @@ int scan_mode(const vbdr *h) {
   return (int)m;
 }
 
+uint8_t *regmax_of(const vbdr *h, uint32_t tick) {
+  return h->regmax_base + (tick & 1u) * h->regmax_stride;
+}
+
 vbdr_launch::EstParams est_params(const vbdr *h) {
   vbdr_launch::EstParams e{};
   const uint32_t closed = h->p.tick - 1u;  // tick of the last boundary (0 = none)
-  e.regmax = h->p.regmax;
-  e.acc = h->p.acc + 2 * (closed & 1u);
+  e.regmax = regmax_of(h, closed);
+  e.acc = h->p.acc + 2 * (closed & 3u);
   e.mask = h->p.mask;
   e.A0 = h->p.A0;
   e.L = h->p.L;
@@ -348,14 +357,15 @@ vbdr_status after_slide(vbdr_t *h, void *stream) {
   h->info.slices_closed += 1;
   h->p.tick += 1;
   if (h->p.tick >= kTickLimit) {
-    // Every stamp is stale after a slide; restart the tick at 2 (same parity
-    // as kTickLimit, so the accumulator slots keep alternating).
+    // Every stamp is stale after a slide; restart the tick at 4 (kTickLimit
+    // mod 4, so the register buffers and accumulator slots keep rotating).
     if (h->fast) {
       const cudaError_t m = cudaMemsetAsync(h->p.sr, 0, 4ull * h->p.n_phys, S(stream));
       if (m != cudaSuccess) return cuda_fail(h, m, "tick wrap");
     }
-    h->p.tick = 2;
+    h->p.tick = 4;
   }
+  h->p.regmax = regmax_of(h, h->p.tick);
   return VBDR_OK;
 }
 
@@ -417,7 +427,9 @@ vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, v
   p.acc = reinterpret_cast<unsigned long long *>(base + pl.off_acc);
   p.sr = h->fast ? reinterpret_cast<uint32_t *>(base + pl.off_sr) : nullptr;
   p.drv = reinterpret_cast<uint32_t *>(base + pl.off_drv);
-  p.regmax = base + pl.off_regmax;
+  h->regmax_base = base + pl.off_regmax;
+  h->regmax_stride = pl.regmax_stride;
+  p.regmax = h->regmax_base;  // k_init clears buffer 0; buffer 1 below
   p.n_phys = h->cfg.n_phys;
   p.drv_n = h->cfg.drv_shards > 1 ? h->cfg.n_phys / h->cfg.drv_shards : h->cfg.n_phys;
   p.drv_j0 = h->cfg.drv_shards > 1 ? p.drv_n * h->cfg.drv_shard : 0;
@@ -458,11 +470,14 @@ vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, v
   in.off_drv = pl.off_drv;
   in.off_regmax = pl.off_regmax;
   in.state_bytes = pl.bytes;
-  const cudaError_t ce = vbdr_launch::init(p, h->fast, S(stream));
+  cudaError_t ce = vbdr_launch::init(p, h->fast, S(stream));
+  if (ce == cudaSuccess)
+    ce = cudaMemsetAsync(h->regmax_base + h->regmax_stride, 0, h->cfg.n_phys, S(stream));
   if (ce != cudaSuccess) {
     delete h;
     return VBDR_ECUDA;
   }
+  p.regmax = regmax_of(h, p.tick);  // the buffer the next slide writes
   in.launches = 1;
   *out = h;
   return VBDR_OK;
@@ -488,6 +503,9 @@ vbdr_status vbdr_info(const vbdr_t *h, vbdr_info_t *info) {
   if (!h || !info) return VBDR_EINVAL;
   *info = h->info;
   info->tick = h->p.tick;
+  // the register buffer of the closed tick, and the one the next slide writes
+  info->off_regmax = h->info.off_regmax + ((h->p.tick - 1u) & 1u) * h->regmax_stride;
+  info->off_regmax_next = h->info.off_regmax + (h->p.tick & 1u) * h->regmax_stride;
   return VBDR_OK;
 }
 
@@ -523,9 +541,10 @@ vbdr_status vbdr_debug_set_tick(vbdr_t *h, uint32_t tick) {
   if (!h) return VBDR_EINVAL;
   if (h->info.slices_closed != 0 || h->p.tick != 1)
     return fail(h, VBDR_ESTATE, "the tick can only be set on a fresh pool");
-  if (tick < 1 || tick >= kTickLimit || (tick & 1u) != 1u)
-    return fail(h, VBDR_EINVAL, "tick must be odd and in [1, 2^26)");
-  h->p.tick = tick;  // fresh pool: every stamp is 0 < tick, accumulator parity kept
+  if (tick < 1 || tick >= kTickLimit || (tick & 3u) != 1u)
+    return fail(h, VBDR_EINVAL, "tick must be 1 mod 4 and in [1, 2^26)");
+  h->p.tick = tick;  // fresh pool: every stamp is 0 < tick, buffers / slots rotation kept
+  h->p.regmax = regmax_of(h, tick);
   return VBDR_OK;
 }
 
@@ -938,7 +957,8 @@ vbdr_status vbdr_export_ages_at(vbdr_t *h, const uint64_t *d_idx, uint64_t n_idx
 vbdr_status vbdr_export_regmax(vbdr_t *h, uint8_t *h_regmax, void *stream) {
   if (!h || !h_regmax) return VBDR_EINVAL;
   cudaStream_t cs = S(stream);
-  cudaError_t e = cudaMemcpyAsync(h_regmax, h->p.regmax, h->p.n_phys, cudaMemcpyDeviceToHost, cs);
+  cudaError_t e = cudaMemcpyAsync(h_regmax, regmax_of(h, h->p.tick - 1u), h->p.n_phys,
+                                  cudaMemcpyDeviceToHost, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e != cudaSuccess) return cuda_fail(h, e, "export_regmax");
   return VBDR_OK;
@@ -949,7 +969,7 @@ vbdr_status vbdr_export_pool_sums(vbdr_t *h, uint64_t *h_S_tot, uint64_t *h_V_to
   const uint32_t closed = h->p.tick - 1u;
   unsigned long long v[2];
   cudaStream_t cs = S(stream);
-  cudaError_t e = cudaMemcpyAsync(v, h->p.acc + 2 * (closed & 1u), sizeof v,
+  cudaError_t e = cudaMemcpyAsync(v, h->p.acc + 2 * (closed & 3u), sizeof v,
                                   cudaMemcpyDeviceToHost, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e != cudaSuccess) return cuda_fail(h, e, "export_pool_sums");

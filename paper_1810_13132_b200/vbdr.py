@@ -38,7 +38,8 @@ class vbdr_info_t(C.Structure):
                 ("fields", C.c_uint32), ("words", C.c_uint32), ("tick", C.c_uint32),
                 ("n_phys", C.c_uint64), ("slices_closed", C.c_uint64), ("off_acc", C.c_uint64),
                 ("off_sr", C.c_uint64), ("off_drv", C.c_uint64), ("off_regmax", C.c_uint64),
-                ("state_bytes", C.c_uint64), ("launches", C.c_uint64)]
+                ("state_bytes", C.c_uint64), ("launches", C.c_uint64),
+                ("off_regmax_next", C.c_uint64)]
 
 
 # Every symbol include/vbdr.h declares (tests check the library exports them).
@@ -211,7 +212,7 @@ class VBDR:
         """(S_tot, V_tot) of the last closed slice as an int64[2] view."""
         import torch
         inf = self.info()
-        off = inf["off_acc"] + 16 * ((inf["tick"] - 1) & 1)
+        off = inf["off_acc"] + 16 * ((inf["tick"] - 1) & 3)
         return self.state[off:off + 16].view(torch.int64)
 
     # --------------------------------------------------------------- the path
@@ -285,8 +286,10 @@ class VBDR:
         """Device address of the accumulator block (vbdr_info off_acc)."""
         return self.state.data_ptr() + self.info()["off_acc"]
 
-    def regmax_ptr(self) -> int:
-        return self.state.data_ptr() + self.info()["off_regmax"]
+    def regmax_ptr(self, next: bool = False) -> int:
+        """Device address of the closed tick's register buffer, or with
+        next=True of the buffer the next slide writes (the two alternate)."""
+        return self.state.data_ptr() + self.info()["off_regmax_next" if next else "off_regmax"]
 
     def estimate(self, hosts, out=None, stream=None):
         """``vbdr_estimate``: hosts is a device uint32/int32 tensor; returns float64."""
@@ -557,7 +560,7 @@ class PeerMerge:
         hs = symm.rendezvous(pool.state, grp)
         inf = pool.info()
         self.peer_delta = [hd.buffer_ptrs[r] for r in range(self.world)]
-        self.peer_regmax = [hs.buffer_ptrs[r] + inf["off_regmax"] for r in range(self.world)]
+        self.peer_base = [hs.buffer_ptrs[r] for r in range(self.world)]
         self.peer_acc = [hs.buffer_ptrs[r] + inf["off_acc"] for r in range(self.world)]
         self.flag = torch.zeros(1, dtype=torch.int32, device=pool.device)
         n = pool.n_phys // self.world
@@ -572,7 +575,10 @@ class PeerMerge:
     def close_slice(self):
         self.pool.stamp_delta(self.delta)
         self._barrier()  # every rank's delta is written
-        self.pool.slide_peers(self.peer_delta, self.j0, self.j1, self.peer_regmax, self.peer_acc)
+        # the register buffer the slide writes alternates with the tick (same on every rank)
+        off = self.pool.info()["off_regmax_next"]
+        peer_regmax = [b + off for b in self.peer_base]
+        self.pool.slide_peers(self.peer_delta, self.j0, self.j1, peer_regmax, self.peer_acc)
         self._barrier()  # every rank's register shard and sums have landed
 
 

@@ -50,19 +50,19 @@ def test_sm100a_code_only(vb):
 
 def test_state_bytes_and_validation(vb):
     cfg = vb.make_config(128, 5, 1 << 22, scan_mode=5)
-    # layout F: acc 256 B + sr 16 MiB + DRV 3 planes * 16 MiB + regmax 4 MiB
-    assert vb.state_bytes(cfg) == 256 + 4 * (1 << 22) + 12 * (1 << 22) + (1 << 22)
+    # layout F: acc 256 B + sr 16 MiB + DRV 3 planes * 16 MiB + two regmax buffers of 4 MiB
+    assert vb.state_bytes(cfg) == 256 + 4 * (1 << 22) + 12 * (1 << 22) + 2 * (1 << 22)
     assert vb.state_bytes(vb.make_config(128, 5, 1 << 22)) == vb.state_bytes(cfg)
     # the binned scan (mode 6) adds 256 bins of 2^23/256 * 9/8 + 512 records + cursors
     bins = 4 * 256 * (32768 + 4096 + 512) + 4 * 256
     assert vb.state_bytes(vb.make_config(128, 5, 1 << 22, scan_mode=6)) == vb.state_bytes(cfg) + bins
     cfgp = vb.make_config(128, 5, 1 << 22, layout="packed")
-    assert vb.state_bytes(cfgp) == 256 + 12 * (1 << 22) + (1 << 22)
+    assert vb.state_bytes(cfgp) == 256 + 12 * (1 << 22) + 2 * (1 << 22)
     # bigwin: zb = 6, F = 5, W = 5
     assert vb.state_bytes(vb.make_config(256, 60, 1 << 28, scan_mode=5)) == \
-        256 + (4 + 20 + 1) * (1 << 28)
+        256 + (4 + 20 + 2) * (1 << 28)
     assert vb.state_bytes(vb.make_config(256, 60, 1 << 28)) == \
-        256 + (4 + 20 + 1) * (1 << 28)
+        256 + (4 + 20 + 2) * (1 << 28)
     bad = [dict(m=3, k=5, n_phys=1 << 10), dict(m=512, k=5, n_phys=1 << 9),
            dict(m=32, k=0, n_phys=1 << 12), dict(m=32, k=4, n_phys=3000),
            dict(m=32, k=8, n_phys=1 << 12, zbits=3), dict(m=32, k=4, n_phys=1 << 12, rank_cap=28),

@@ -230,6 +230,41 @@ def test_sparse_extract_counts_and_cap():
         pool.sparse_extract(3)  # 4096 BDRs do not split in 3
 
 
+@pytest.mark.parametrize("layout", ["fast", "packed"])
+def test_estimate_overlapping_next_slide(layout):
+    """Two register buffers and four pool-sum slots: the estimate of slice t
+    (second stream) may run while slice t+1 is scanned and slid; every
+    slice's estimates still equal the oracle's at that boundary."""
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(32, 4, 1 << 12, layout=layout, device=DEV)
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    plan = pool.plan(hosts)
+    main, side = torch.cuda.current_stream(DEV), torch.cuda.Stream(DEV)
+    ev_closed, ev_est = torch.cuda.Event(), [torch.cuda.Event(), torch.cuda.Event()]
+    slices = [synth.generate(tr, t) for t in range(9)]
+    dev_slices = [dev_u32(p) for p in slices]
+    outs = [torch.empty(len(hosts_np), dtype=torch.float64, device=DEV) for _ in slices]
+    pool.scan_slice(dev_slices[0])
+    pool.slide()
+    for t in range(len(slices)):
+        ev_closed.record(main)
+        side.wait_event(ev_closed)
+        pool.estimate_plan(plan, out=outs[t], stream=side)  # slice t
+        ev_est[t & 1].record(side)
+        if t + 1 < len(slices):
+            pool.scan_slice(dev_slices[t + 1])
+            main.wait_event(ev_est[(t - 1) & 1])
+            pool.slide()  # slice t+1, concurrent with the estimate of slice t
+    torch.cuda.synchronize()
+    for t, pairs in enumerate(slices):
+        ref.slice(pairs)
+        M = ref.readout()
+        check_estimates(outs[t].cpu().numpy(), ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
+
+
 def test_register_sharded_state_rules():
     """drv_shards: the DRV of one shard only; closing or exporting the whole
     pool is refused, slide_delta outside the shard is refused."""
@@ -483,7 +518,7 @@ def test_tick_wraparound(layout):
     cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
     ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
     pool = VBDR(32, 4, 1 << 12, layout=layout, device=DEV)
-    pool.debug_set_tick((1 << 26) - 5)
+    pool.debug_set_tick((1 << 26) - 7)  # 1 mod 4: register buffers / sum slots rotate
     hosts_np = tr.host_ids()
     for t in range(10):
         pairs = synth.generate(tr, t)
@@ -533,11 +568,11 @@ def test_loopback_fused_peer_merge_slide(n_ranks):
     ranks = [VBDR(32, 4, 1 << 12, device=DEV) for _ in range(n_ranks)]
     deltas = [torch.empty(cfg.z, dtype=torch.uint8, device=DEV) for _ in range(n_ranks)]
     n = cfg.z // n_ranks
-    regmax = [p.regmax_ptr() for p in ranks]
     acc = [p.acc_ptr() for p in ranks]
     hosts_np = tr.host_ids()
     for t in range(7):
         pairs = synth.generate(tr, t)
+        regmax = [p.regmax_ptr(next=True) for p in ranks]  # alternates with the tick
         for r, pool in enumerate(ranks):
             a, b = shard_range(len(pairs), r, n_ranks)
             pool.scan_slice(dev_u32(pairs[a:b]))
