@@ -534,8 +534,9 @@ def run_vbdr(args):
         h_inputs = [inputs[i].cpu().pin_memory() for i in range(min(n_inputs, 4))]
         h_hosts = torch.from_numpy(hosts_all[h0:h1].view(np.int32)).pin_memory()
         h_out = torch.empty(h1 - h0, dtype=torch.float64).pin_memory()
-        # two halves of a whole slice each: the next slice's copy overlaps this slice's compute
-        stage = torch.empty(2 * 2 * n_local, dtype=torch.int32, device=dev)
+        # two slots of half a slice each: the scan of one half overlaps the copy of
+        # the next (tools/e2e_probe.py: 0.742 ms/step vs 0.779 with whole-slice slots)
+        stage = torch.empty(2 * n_local, dtype=torch.int32, device=dev)
         hstage = torch.empty(max(h1 - h0, 1), dtype=torch.int32, device=dev)
         ostage = torch.empty(max(h1 - h0, 1), dtype=torch.float64, device=dev)
 

@@ -49,3 +49,17 @@ run("full e2e step", lambda i: (pool.scan_slice_host(h_in[i % 4], stage), pool.s
                                 pool.estimate_host(h_hosts, hs, os_, h_out)))
 run("device-resident step (no copies)", lambda i: (pool.scan_slice(d_in), pool.slide(),
                                                    pool.estimate(hs, out=os_)))
+plan = pool.plan(torch.from_numpy(hosts.view(np.int32)).to(dev))
+run("e2e step, plan estimate + D2H", lambda i: (pool.scan_slice_host(h_in[i % 4], stage), pool.slide(),
+                                               pool.estimate_plan_host(plan, os_, h_out)))
+run("e2e step, plan estimate, no D2H", lambda i: (pool.scan_slice_host(h_in[i % 4], stage), pool.slide(),
+                                                 pool.estimate_plan(plan, out=os_)))
+small = torch.empty(2 * n, dtype=torch.int32, device=dev)  # half-slice chunks
+run("e2e step, half-slice chunks", lambda i: (pool.scan_slice_host(h_in[i % 4], small), pool.slide(),
+                                             pool.estimate_plan_host(plan, os_, h_out)))
+quarter = torch.empty(n, dtype=torch.int32, device=dev)  # quarter-slice chunks
+run("e2e step, quarter-slice chunks", lambda i: (pool.scan_slice_host(h_in[i % 4], quarter), pool.slide(),
+                                                pool.estimate_plan_host(plan, os_, h_out)))
+eighth = torch.empty(n // 2, dtype=torch.int32, device=dev)
+run("e2e step, eighth-slice chunks", lambda i: (pool.scan_slice_host(h_in[i % 4], eighth), pool.slide(),
+                                               pool.estimate_plan_host(plan, os_, h_out)))
