@@ -13,8 +13,8 @@ namespace vbdr_dev {
 struct DevParams {
   uint32_t *sr;              // u32[n_phys] stamp words (layout F)
   uint32_t *drv;             // u32[W][drv_n] packed DRV of BDRs [drv_j0, drv_j0 + drv_n), plane-major
-  uint8_t *regmax;           // u8[n_phys] register values M[j]
-  unsigned long long *acc;   // u64[4]: (S_tot, V_tot) per tick parity
+  uint8_t *regmax;           // u8[n_phys] register values M[j]: the buffer the next slide writes
+  unsigned long long *acc;   // u64[8]: (S_tot, V_tot) per tick mod 4
   uint64_t n_phys;
   uint64_t drv_j0, drv_n;    // the DRV shard (0, n_phys unless register-sharded)
   uint32_t mask;             // n_phys - 1 (n_phys <= 2^32)
