@@ -628,7 +628,10 @@ def run_vbdr(args):
             "peak": hbm, "unit": "GB/s", "frac": round(plan_gbs / hbm, 4),
             "algorithmic_bytes": plan_bytes, "traffic": traffic.get("estimate_plan"),
             "gathers_per_s": round(g_rate * 1e9), "hosts": h1 - h0, "gathers": gathers,
-            "peak_source": hbm_src}
+            "peak_source": hbm_src,
+            "note": "HBM is not what binds it: the two-stage TMA block pipeline does "
+                    "(block streaming without compute takes ~85 % of its time; "
+                    "profiles/r01_plan_variants.txt)"}
     dominant = max(("scan", "slide", "estimate"), key=lambda n: kern[n])
     roof = {"kernel": dominant, **{k: v for k, v in kernels[dominant].items() if k != "ms"}}
 
