@@ -84,6 +84,23 @@ def _worker(rank, world, port, q):
         regs[rank * n:(rank + 1) * n] = shard
         all_gather_shards(regs)
         ok &= np.array_equal(regs.numpy(), whole.now())
+        # sparse exchange plumbing (slide_merged 'sparse'): per-owner records of
+        # the touched BDRs ((j - owner start) << 5 | rank), counts then records
+        # all-to-all, folded into the owner's shard with a per-byte max
+        from paper_1810_13132_b200.vbdr import _all_to_all
+        now = mine.now()
+        recs = [np.array([((j - o * n) << 5) | int(now[j]) for j in np.flatnonzero(now[o * n:(o + 1) * n]) + o * n],
+                         dtype=np.int32) for o in range(world)]
+        counts = torch.tensor([len(r) for r in recs], dtype=torch.int64)
+        recv_counts = torch.empty_like(counts)
+        _all_to_all(recv_counts, counts, None, None)
+        send = torch.from_numpy(np.concatenate(recs))
+        recv = torch.empty(int(recv_counts.sum()), dtype=torch.int32)
+        _all_to_all(recv, send, recv_counts.tolist(), counts.tolist())
+        folded = np.zeros(n, np.uint8)
+        r = recv.numpy().view(np.uint32)
+        np.maximum.at(folded, (r >> 5).astype(np.int64), (r & 31).astype(np.uint8))
+        ok &= np.array_equal(folded, whole.now()[rank * n:(rank + 1) * n])
         # max-over-ranks timing reduction used by bench.py
         t_local = torch.tensor([1.0 + rank], dtype=torch.float64)
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
