@@ -78,6 +78,16 @@ def test_state_bytes_and_validation(vb):
         vb.state_bytes(vb.make_config(32, 7, 1 << 12, zbits=3, layout="packed"))
 
 
+def test_register_sharded_state_bytes_and_validation(vb):
+    full = vb.state_bytes(vb.make_config(128, 5, 1 << 22, scan_mode=5))
+    sharded = vb.state_bytes(vb.make_config(128, 5, 1 << 22, scan_mode=5, drv_shards=4, drv_shard=3))
+    assert full - sharded == 12 * (1 << 22) * 3 // 4  # 3 DRV planes, 3/4 of the BDRs gone
+    for kw in (dict(drv_shards=4, drv_shard=4), dict(drv_shards=0, drv_shard=1),
+               dict(drv_shards=3), dict(drv_shards=2, layout="packed")):
+        with pytest.raises(ValueError, match="invalid VBDR config: "):
+            vb.state_bytes(vb.make_config(128, 5, 1 << 22, **kw))
+
+
 def test_shard_range_partitions():
     from paper_1810_13132_b200 import shard_range
     for n in (0, 1, 7, 100, 5_000_001):
