@@ -470,6 +470,35 @@ def run_vbdr(args):
         step(i)
     barrier()
 
+    # --estimate auto: the plan streams the whole register array through every
+    # SM whatever the host count, the gather scales with the hosts; keep the
+    # faster of the two for this rank's host share (same results either way)
+    est_choice = None
+    if args.estimate == "auto" and plan is not None:
+        def time_est(use_plan):
+            evs = [(E(), E()) for _ in range(5)]
+            for j in range(7):
+                flush.fill_(j & 0xFF)
+                if j >= 2:
+                    evs[j - 2][0].record(stream)
+                if use_plan:
+                    pool.estimate_plan(plan, out=est_out)
+                else:
+                    pool.estimate(hosts, out=est_out)
+                if j >= 2:
+                    evs[j - 2][1].record(stream)
+            torch.cuda.synchronize()
+            return float(np.median([a.elapsed_time(b) for a, b in evs]))
+        t_plan, t_gather = time_est(True), time_est(False)
+        if world > 1:  # one choice for every rank: the slowest rank decides
+            t = torch.tensor([t_plan, t_gather], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_plan, t_gather = float(t[0]), float(t[1])
+        est_choice = {"plan_ms": round(t_plan, 5), "gather_ms": round(t_gather, 5)}
+        if t_gather < t_plan:
+            plan = None
+        barrier()
+
     # ---- device-resident timed region (clocks sampled through it and the e2e region)
     clocks = ClockSampler(gpu) if rank == 0 else None
     if clocks:
@@ -665,6 +694,7 @@ def run_vbdr(args):
                                      "plan (shared-memory staged)" if staged else
                                      "plan (pass ids, multi-pass gather)"),
                    "plan_build_ms": round(plan_build_ms, 2) if plan_build_ms else None,
+                   "estimate_autotune": est_choice,
                    "plan_bytes": plan.nbytes if plan is not None else None,
                    "zbits": info["zbits"], "words_per_bdr": info["words"],
                    "bits_per_bdr": (32 if args.layout == "fast" else 0) + 32 * info["words"],
