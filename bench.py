@@ -408,12 +408,7 @@ def run_vbdr(args):
             pool.slide()
             mark(evs, 3)
         elif args.merge == "p2p":
-            pool.stamp_delta(peer.delta)
-            peer._barrier()
-            mark(evs, 2)
-            pool.slide_peers(peer.peer_delta, peer.j0, peer.j1, peer.peer_regmax, peer.peer_acc)
-            mark(evs, 3)
-            peer._barrier()
+            peer.close_slice(on_merged=lambda: mark(evs, 2), on_slid=lambda: mark(evs, 3))
         elif args.merge == "sparse":
             slide_merged(pool, group, "sparse", shard=shard_buf)
             mark(evs, 2)
@@ -602,6 +597,12 @@ def run_vbdr(args):
                "timing": "one CUDA-event region over all steps, copies pipelined across steps"}
 
     clk = clocks.stop() if clocks else None
+    # a staged plan transfer that timed out leaves NaN estimates and sets the
+    # plan's error flag: never report a number from such a run
+    if plan is not None:
+        pool.plan_check(plan)  # raises (non-zero exit) if any timed estimate failed
+    if bool(torch.isnan(est_out).any()):
+        raise SystemExit("bench: NaN estimates (a failed plan estimate)")
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

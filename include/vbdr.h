@@ -79,18 +79,11 @@ typedef struct {
     uint32_t rank_cap;
     /* layout: vbdr_layout. */
     uint32_t layout;
-    /* scan_mode: 0 = default; 1 = plain atomic per pair; 2 = L2 load-check,
-     * skip the atomic when the stored value already dominates; 3 = warp-
-     * aggregated atomic (lanes with the same word combine their update,
-     * one lane checks L2 and issues it); 4 = L1-cached load-check; 5 = per-block shared-memory
-     * cache of recently updated words in front of the mode-2 check (the
-     * default for layout fast; 2 for packed); 6 = binned (layout fast,
-     * n_phys <= 2^26, else runs as 5; measured slower than 5): pairs are
-     * partitioned into per-bucket bins of 2^14 BDRs, then each bucket's
-     * max ranks are formed in shared memory and merged into its stamp words
-     * with coalesced stores (the state buffer grows by the bins, about
-     * 4.5 * min(2 n_phys, 2^27) bytes).  All modes give bit-identical state
-     * (stored values only move one way within a slice). */
+    /* scan_mode: 0 = default (5 for layout fast, 2 for packed); 2 = L2
+     * load-check, skip the atomic when the stored value already dominates;
+     * 5 = a per-block shared-memory cache of recently updated words in front
+     * of the mode-2 check.  Other values: VBDR_EINVAL.  Both modes give
+     * bit-identical state (stored values only move one way within a slice). */
     uint32_t scan_mode;
     /* est_lanes: lanes cooperating on one host in vbdr_estimate (1, 2, 4, 8,
      * 16 or 32; 0 = auto).  Tuning only; results are identical. */
@@ -222,9 +215,12 @@ vbdr_status vbdr_sparse_apply(vbdr_t *h, const uint32_t *d_records, uint64_t n_r
  * rank, each to that rank's u8[n_phys] delta from vbdr_stamp_delta -- local or
  * mapped over NVLink (CUDA IPC / symmetric memory).  The kernel merges the
  * deltas of BDRs [j0, j1) with a per-byte max while sliding them.  If
- * h_peer_regmax (n_peers pointers to every rank's regmax, vbdr_info
- * off_regmax) is given, the register shard is written into every rank's
- * regmax instead of only the local one; if h_peer_acc (n_peers pointers to
+ * h_peer_regmax is given -- n_peers pointers to the register buffer every
+ * rank's NEXT slide writes, i.e. base + vbdr_info off_regmax_next read BEFORE
+ * this call (the two register buffers alternate with the tick; off_regmax is
+ * the closed tick's buffer and is wrong here) -- the register shard is written
+ * into every rank's buffer instead of only the local one; VBDR_EINVAL if no
+ * entry equals this handle's own next buffer.  If h_peer_acc (n_peers pointers to
  * every rank's accumulator base, vbdr_info off_acc) is given, the shard's pool
  * sums are added atomically into every rank (own rank included in both
  * lists).  The caller orders it between two cross-rank barriers: after every
@@ -255,33 +251,56 @@ vbdr_status vbdr_host_sums(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
 vbdr_status vbdr_select_above(vbdr_t *h, const double *d_est, uint64_t n, double threshold,
                               uint32_t *d_idx, uint64_t *d_count, void *stream);
 
-/* ---- plan-based estimation (a fixed host list, pools up to 2^22 BDRs) -- */
+/* ---- plan-based estimation (a fixed host list) ------------------------ */
 
-/* The gather estimate reads each register with its own L2 sector request.  A
- * PLAN preprocesses a host list once: every (host, i) gather of Alg.5 is
- * precomputed and grouped by 64 KB block of the register array and by warp,
- * as rounds of 32 entries; per slice the estimate then streams the array block
- * by block through shared memory (TMA bulk copies) and every lane adds one
- * register per round into its host's shared-memory accumulator.  Same integer
- * sums, same fp64 finish: results are bit-identical to vbdr_estimate.  Needs
- * n_phys in [64, 2^22], n_hosts <= 7 * 512 * SMs (530k on B200) and
- * g * 2^(L-1) (HLL) or g * 255 below 2^32.
- * Larger pools whose gather estimate runs in 2..4 passes (est_pass_log2)
- * with 64 <= g <= 2048 get a PASS-ID plan instead: a copy of the host list
- * and the pass of every (host, i) in 2 bits, so each pass hashes and gathers
- * only its own registers (same sums, bit-identical).  Otherwise VBDR_ERANGE. */
+/* The gather estimate (vbdr_estimate) reads each register of Alg.5
+ * with its own L2 sector request: the (host, i) indices of
+ * Alg.3 are random.  A PLAN preprocesses a host list once
+ * (the monitored hosts) so that every later estimate reads the same registers
+ * in a cheaper order.  All kinds produce the same integer sums and the same
+ * fp64 finish: results are bit-identical to vbdr_estimate.  Kinds:
+ *  - VBDR_PLAN_SORTED (k_splan.cu): every (host, i) listed once, sorted by
+ *    register line, per CTA of a grid of P host groups x C register ranges;
+ *    each CTA keeps its group's (S', V) in shared memory (8 B per host), so
+ *    needs ceil(n_hosts / P) * 8 B <= the SM's shared memory (with C = 1:
+ *    about 4.2 M hosts on 148 SMs), g * 2^(L-1) (HLL) or g * 255 below 2^32,
+ *    n_phys >= 128.  Plan: 4 B per (host, i) plus the bucket table
+ *    (n_phys * P / 128 * 4 B).  One estimate per plan at a time (stream-ordered).
+ *  - VBDR_PLAN_STAGED (k_plan.cu): the register array streamed through shared
+ *    memory in 64 KB blocks by TMA, (host, i) entries grouped by block and
+ *    warp in bank-scheduled rounds; n_phys in [64, 2^22], n_hosts <= 7 * 512
+ *    * SMs.
+ *  - VBDR_PLAN_PASSID (k_estimate.cu): for pools whose gather estimate runs
+ *    in 2..4 passes (est_pass_log2), 64 <= g <= 2048: the pass of every
+ *    (host, i) in 2 bits, so each pass hashes and gathers only its registers.
+ * VBDR_PLAN_AUTO takes the first that fits in the order SORTED, STAGED,
+ * PASSID; otherwise VBDR_ERANGE. */
+typedef enum {
+    VBDR_PLAN_AUTO = 0,
+    VBDR_PLAN_STAGED = 1,
+    VBDR_PLAN_PASSID = 2,
+    VBDR_PLAN_SORTED = 3
+} vbdr_plan_kind;
 
-/* SYNC, host only.  Bytes of the caller's plan buffer for n_hosts hosts. */
+/* SYNC, host only.  Bytes of the caller's plan buffer for n_hosts hosts
+ * (VBDR_PLAN_AUTO); VBDR_ERANGE if no kind fits. */
 vbdr_status vbdr_plan_bytes(const vbdr_t *h, uint64_t n_hosts, uint64_t *bytes);
+
+/* vbdr_plan_bytes for one kind (vbdr_plan_kind). */
+vbdr_status vbdr_plan_bytes_kind(const vbdr_t *h, uint64_t n_hosts, uint32_t kind,
+                                 uint64_t *bytes);
 
 /* SYNC.  Build the plan for d_hosts (u32[n_hosts], kept by the plan only as
  * indices: later estimates report host j at position j) into d_plan
- * (256-byte aligned, >= vbdr_plan_bytes).  VBDR_ERANGE if a register block
- * would hold more entries than one shared-memory stage (then use
- * vbdr_estimate).  The plan belongs to this handle and stays valid until
- * vbdr_plan_release or the handle is destroyed. */
+ * (256-byte aligned, >= vbdr_plan_bytes), kind VBDR_PLAN_AUTO.  VBDR_ERANGE
+ * if no kind fits (then use vbdr_estimate).  The plan belongs to this handle
+ * and stays valid until vbdr_plan_release or the handle is destroyed. */
 vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, void *d_plan,
                             uint64_t bytes, void *stream);
+
+/* vbdr_plan_build of one kind (vbdr_plan_kind; bytes from vbdr_plan_bytes_kind). */
+vbdr_status vbdr_plan_build_kind(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
+                                 uint32_t kind, void *d_plan, uint64_t bytes, void *stream);
 
 /* vbdr_estimate for the plan's hosts (d_out f64[n_hosts]). */
 vbdr_status vbdr_estimate_plan(vbdr_t *h, const void *d_plan, double *d_out, void *stream);
@@ -296,7 +315,9 @@ vbdr_status vbdr_host_sums_plan(vbdr_t *h, const void *d_plan, uint64_t *d_S, ui
                                 void *stream);
 
 /* SYNC.  VBDR_ECUDA if a plan estimate on this plan ever timed out waiting for
- * a staged transfer (never expected; the kernel stops instead of hanging). */
+ * a staged transfer (VBDR_PLAN_STAGED only; never expected: the kernel stops
+ * instead of hanging and writes NaN estimates, or all-ones sums, for the hosts
+ * it could not finish -- never a stale value). */
 vbdr_status vbdr_plan_check(vbdr_t *h, const void *d_plan, void *stream);
 
 /* Forget a plan (the caller frees its buffer). */

@@ -31,6 +31,7 @@ SOURCES = [
     ("k_scan_slide.cu", []),
     ("k_estimate.cu", ["-fmad=false"]),
     ("k_plan.cu", ["-fmad=false"]),
+    ("k_splan.cu", ["-fmad=false"]),
     ("vbdr_host.cu", []),
 ]
 

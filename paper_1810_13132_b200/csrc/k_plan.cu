@@ -433,11 +433,13 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
   uint32_t *accv = acc + kAccW;
   const uint32_t acc_base = smem_u32(acc);
   const uint32_t K = 1u << e.L;  // 2^(L - M) = K >> M
+  bool ok = true;  // a staged transfer that never lands poisons this warp's hosts (NaN)
   for (uint32_t ph = 0; ph < phases; ++ph) {
     const int b = ph & 1;
     if (!mbar_wait(&sm.full[b], (ph >> 1) & 1u)) {
       if (lane == 0) atomicAdd(err, 1ull);
-      return;
+      ok = false;
+      break;
     }
     const uint8_t *tab = sm.tab[b];
     const uint32_t r0 = sm.start[b][w], r1 = sm.start[b][w + 1];
@@ -473,12 +475,22 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
     const uint64_t h = slot_host(blockIdx.x, w, lane, s, gridDim.x);
+    // (a warp that timed out still writes its hosts: NaN below)
     if (h >= n) break;
     const uint32_t Sp = acc[s * 32 + lane], Vz = accv[s * 32 + lane];
     // HLL: Vz = V 2^L mod 2^32, which wraps only for V = g when g 2^L = 2^32,
     // i.e. every register zero -- exactly when S' = 0 (each M >= 1 adds >= 1)
     const uint32_t V = HLL ? (Sp == 0u ? e.g : Vz >> e.L) : Vz;
     const unsigned long long S = Sp + (HLL ? (unsigned long long)V << e.L : 0ull);
+    if (!ok) {  // loud: never a stale value from an earlier slice
+      if constexpr (SUMS) {
+        outS[h] = ~0ull;
+        outV[h] = ~0u;
+      } else {
+        out[h] = __longlong_as_double(0x7FF8000000000000ll);  // NaN
+      }
+      continue;
+    }
     if constexpr (SUMS) {
       outS[h] = S;
       outV[h] = V;

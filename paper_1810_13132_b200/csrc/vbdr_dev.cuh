@@ -22,12 +22,6 @@ struct DevParams {
   uint32_t A0, A1;
   uint32_t tick;             // T of the open slice
   uint32_t est;              // register estimator: 0 HLL, 1 LogLog, 2 PCSA (packed only)
-  // binned scan (scan_mode 6, layout F): per-bucket record bins
-  uint32_t *bins;            // u32[n_bkt][bcap]: (offset in bucket << 5) | rho
-  uint32_t *bcursor;         // u32[n_bkt] fill counts (zero between chunks)
-  uint32_t bkt_log2;         // BDRs per bucket = 2^bkt_log2
-  uint32_t bcap;             // records per bucket
-  uint64_t bchunk;           // pairs per bin + apply round
 };
 
 // H(x, 2^32, A) = fmix32(x ^ A) (R#6: MurmurHash3 finaliser).
@@ -195,8 +189,16 @@ constexpr int kPlanThreads = 512;
 constexpr int kPlanSlots = 7;     // hosts per thread (accumulator slots per lane)
 constexpr int kPlanEntCap = 8192; // entries per (CTA, block) staged in shared memory
 constexpr int kPlanStride = 20;   // round starts per (CTA, block): 16 warps + total, 16-byte padded
+// Sorted plan (k_splan.cu): entries sorted by register line, P host groups x
+// C register ranges, one CTA per SM.
+constexpr int kSpThreads = 1024;
+constexpr uint32_t kSpLineLog2 = 7;  // bucket = one 128-byte line of registers
+#ifndef VBDR_SP_UNROLL
+#define VBDR_SP_UNROLL 4
+#endif
+constexpr int kSpUnroll = VBDR_SP_UNROLL;
 struct PlanLayout {
-  uint32_t kind;         // 0: shared-memory staged rounds (k_plan.cu); 1: pass ids
+  uint32_t kind;         // 0: shared-memory staged rounds (k_plan.cu); 1: pass ids; 2: sorted (k_splan.cu)
   uint32_t ctas, phases, block_log2;
   uint64_t n_hosts;
   uint32_t *hosts;       // kind 1: a copy of the host list
@@ -209,11 +211,30 @@ struct PlanLayout {
   uint32_t *entries;
   uint32_t *max_range;   // build: largest (CTA, block) entry count
   unsigned long long *error;  // estimate: set if a staged transfer never landed
+  // kind 2 (sorted plan); counts = bucket cursors, range_size = segment totals
+  uint32_t sp_C;           // register ranges per host group
+  uint32_t sp_hpg;         // accumulator slots per group (hosts / P, rounded up)
+  uint32_t sp_nseg;        // segments per CTA range
+  uint32_t sp_SB;          // slot bits of an entry
+  uint32_t sp_seg_log2;    // registers per segment = 2^sp_seg_log2
+  uint32_t sp_range_log2;  // registers per CTA range = z / C
+  uint32_t *sp_segbase;    // [ctas * nseg + 1] first entry of each segment
+  unsigned long long *sp_part;  // [ctas * hpg] partial (S', V) (C > 1)
+  uint32_t *sp_gcount;     // [P] arrivals per group (C > 1)
 };
 cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, uint32_t g,
                        uint32_t A0, uint32_t mask, uint32_t *range_size_scratch, cudaStream_t s);
 cudaError_t estimate_plan(const EstParams &e, const PlanLayout &pl, uint64_t n, double *out,
                           unsigned long long *outS, uint32_t *outV, cudaStream_t s);
+
+size_t sp_smem_bytes(uint32_t hpg, uint32_t nseg);
+// count + segment scan + segment bases (total entries incl. padding -> *d_total), then fill
+cudaError_t sp_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, uint32_t g,
+                     uint32_t A0, uint32_t mask, unsigned long long *d_total, cudaStream_t s);
+cudaError_t sp_fill(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, uint32_t g,
+                    uint32_t A0, uint32_t mask, cudaStream_t s);
+cudaError_t estimate_sp(const EstParams &e, const PlanLayout &pl, uint64_t n, double *out,
+                        unsigned long long *outS, uint32_t *outV, cudaStream_t s);
 
 // Pass-id plan for multi-pass gather estimates (k_estimate.cu): 2 bits per
 // (host, i), 16 bytes per (host, lane), g / 64 lanes per host.

@@ -87,19 +87,14 @@ double alpha_of(uint64_t s) {
 struct StateLayout {
   uint32_t b, L, zb, F, W;
   uint64_t off_acc, off_sr, off_drv, off_regmax, regmax_stride, bytes;
-  // binned scan (scan_mode 6): bins + cursors, 0 bytes otherwise
-  uint32_t bkt_log2 = 0, bcap = 0;
-  uint64_t bchunk = 0, off_bins = 0, off_bcursor = 0;
 };
 
-// scan_mode 0 = default: 5 for layout F, 2 for layout P; mode 6 (binned)
-// only on request and for pools of at most 2^26 BDRs (4096 buckets), else 5
-// (profiles/r01_scan_modes.txt: binned is slower at caida and 10G).
+// scan_mode 0 = default: 5 for layout F, 2 for layout P
+// (profiles/r01_scan_modes.txt; the slower modes 1, 3, 4 and 6 of round 1
+// are recorded in tools/rejected/, not built).
 uint32_t effective_scan_mode(const vbdr_config &n) {
   const bool fast = n.layout != VBDR_LAYOUT_PACKED;
-  uint32_t m = n.scan_mode ? n.scan_mode : (fast ? 5u : 2u);
-  if (m == 6 && (!fast || n.n_phys > (1ull << 26))) m = fast ? 5u : 2u;
-  return m;
+  return n.scan_mode ? n.scan_mode : (fast ? 5u : 2u);
 }
 
 // Validate a config and lay out the state buffer.  Returns an error text or
@@ -112,7 +107,8 @@ std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *p
     n.seed_a1 = 0x5EED0002u;
   }
   if (n.layout > 1) return "layout must be 0 (fast) or 1 (packed)";
-  if (n.scan_mode > 6) return "scan_mode must be 0..6";
+  if (n.scan_mode != 0 && n.scan_mode != 2 && n.scan_mode != 5)
+    return "scan_mode must be 0 (default), 2 (L2 check) or 5 (block cache + L2 check)";
   if (n.est_lanes > 32 || (n.est_lanes & (n.est_lanes - 1)))
     return "est_lanes must be 0 or a power of two <= 32";
   if (n.est_pass_log2 > 32) return "est_pass_log2 must be 0..32";
@@ -164,18 +160,6 @@ std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *p
   pl->off_regmax = off;  // two register buffers: the slide of tick T writes buffer T & 1
   pl->regmax_stride = align256(n.n_phys);
   off = align256(off + 2 * pl->regmax_stride);
-  if (effective_scan_mode(n) == 6) {
-    // buckets of 2^14 BDRs (64 KB of ranks in shared memory); chunks of up to
-    // 2 n_phys pairs (<= 2^27); bins sized for the mean load + 12.5 % + 512
-    pl->bkt_log2 = log2u(n.n_phys) < 14 ? log2u(n.n_phys) : 14u;
-    const uint64_t n_bkt = n.n_phys >> pl->bkt_log2;
-    pl->bchunk = 2ull * n.n_phys < (1ull << 27) ? 2ull * n.n_phys : (1ull << 27);
-    pl->bcap = (uint32_t)(pl->bchunk / n_bkt + pl->bchunk / n_bkt / 8 + 512);
-    pl->off_bins = off;
-    off = align256(off + 4ull * n_bkt * pl->bcap);
-    pl->off_bcursor = off;
-    off = align256(off + 4ull * n_bkt);
-  }
   pl->bytes = off;
   pl->b = b;
   pl->L = L;
@@ -207,15 +191,11 @@ cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 // scan_mode 0 picks the default (effective_scan_mode).
 int scan_mode(const vbdr *h);
 
-// kernels one scan call of n pairs launches (mode 6: bin + apply per chunk)
-uint64_t scan_launches(const vbdr *h, uint64_t n) {
-  if (scan_mode(h) != 6) return 1;
-  return 2 * ((n + h->p.bchunk - 1) / h->p.bchunk);
-}
+// kernels one scan call launches
+uint64_t scan_launches(const vbdr *, uint64_t) { return 1; }
 
 int scan_mode(const vbdr *h) {
   const uint32_t m = effective_scan_mode(h->cfg);
-  if (m == 6) return h->p.bins ? 6 : 5;
   // mode 5 keys its shared-memory cache by word index: fast needs n_phys < 2^32,
   // packed n_phys <= 2^28 (and W <= 15); otherwise use mode 2
   if (m == 5 && (h->fast ? h->p.n_phys >= (1ull << 32) : (h->p.n_phys > (1ull << 28) || h->p.W > 15)))
@@ -444,18 +424,6 @@ vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, v
   p.A1 = h->cfg.seed_a1;
   p.tick = 1;  // slice t = 0 is open, T = t + 1
   p.est = h->cfg.estimator;
-  if (pl.bcap) {
-    p.bins = reinterpret_cast<uint32_t *>(base + pl.off_bins);
-    p.bcursor = reinterpret_cast<uint32_t *>(base + pl.off_bcursor);
-    p.bkt_log2 = pl.bkt_log2;
-    p.bcap = pl.bcap;
-    p.bchunk = pl.bchunk;
-    if (cudaMemsetAsync(p.bcursor, 0, 4ull * (h->cfg.n_phys >> pl.bkt_log2), S(stream)) !=
-        cudaSuccess) {
-      delete h;
-      return VBDR_ECUDA;
-    }
-  }
   h->alpha_g = alpha_of(h->cfg.m);
   h->alpha_z = alpha_of(h->cfg.n_phys);
   vbdr_info_t &in = h->info;
@@ -634,6 +602,14 @@ vbdr_status vbdr_slide_peers(vbdr_t *h, const uint8_t *const *h_peer_delta, uint
   }
   pe.n_regmax = h_peer_regmax ? n_peers : 0;
   pe.n_acc = h_peer_acc ? n_peers : 0;
+  if (h_peer_regmax) {  // the local entry must be the buffer this slide writes (off_regmax_next)
+    bool own = false;
+    for (uint32_t r = 0; r < n_peers; ++r) own = own || pe.regmax[r] == h->p.regmax;
+    if (!own)
+      return fail(h, VBDR_EINVAL,
+                  "h_peer_regmax holds no pointer to this handle's next register buffer "
+                  "(vbdr_info off_regmax_next)");
+  }
   if (vbdr_status s = check_async(h, "before slide_peers")) return s;
   const cudaError_t e = vbdr_launch::slide_peers(h->p, pe, j0, j1, S(stream));
   if (e != cudaSuccess) return cuda_fail(h, e, "slide_peers launch");
@@ -650,6 +626,92 @@ vbdr_status vbdr_select_above(vbdr_t *h, const double *d_est, uint64_t n, double
   if (e != cudaSuccess) return cuda_fail(h, e, "select_above");
   h->info.launches += n ? 1 : 0;
   return VBDR_OK;
+}
+
+// Sorted plan (k_splan.cu): P host groups x C register ranges over the SMs,
+// the group's accumulators in shared memory; the largest C (fewest reads of
+// the register array) whose accumulators fit.
+struct SpGeom {
+  uint32_t ctas, C, P, hpg, SB, range_log2, seg_log2, nseg;
+  uint64_t nbuckets, nkeys, off_offs, off_segtot, off_segbase, off_part, off_gcount, off_misc,
+      off_entries, bytes;
+};
+
+bool sp_geom(const vbdr *h, uint64_t n_hosts, SpGeom *g) {
+  const uint64_t z = h->p.n_phys;
+  if (n_hosts == 0 || z < 128) return false;
+  const uint64_t smax =
+      (uint64_t)h->cfg.m * (h->cfg.estimator == 0 ? 1ull << (h->p.L - 1) : 255ull);
+  if (smax >> 32) return false;  // S' per host accumulates in a u32
+  int sms = 0, dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (sms <= 0) sms = 148;
+  if (optin <= 0) optin = 227 * 1024;
+  const uint64_t budget = (uint64_t)optin - 64;  // static shared memory of the kernel
+  for (uint32_t C = 4; C >= 1; C >>= 1) {
+    if ((uint32_t)sms % C || z / C < 128) continue;
+    const uint32_t P = (uint32_t)sms / C;
+    const uint64_t hpg = (n_hosts + P - 1) / P;
+    uint32_t SB = 1;
+    while ((1ull << SB) < hpg + 32) ++SB;
+    const uint32_t range_log2 = log2u(z / C);
+    uint32_t seg_log2 = 32u - SB < range_log2 ? 32u - SB : range_log2;
+    if (seg_log2 < vbdr_launch::kSpLineLog2) continue;
+    const uint64_t nseg = 1ull << (range_log2 - seg_log2);
+    if (vbdr_launch::sp_smem_bytes((uint32_t)hpg, (uint32_t)nseg) > budget) continue;
+    const uint64_t nkeys = (uint64_t)sms * nseg;
+    if (n_hosts * h->cfg.m + 31 * nkeys >= (1ull << 32)) return false;  // u32 entry offsets
+    g->ctas = (uint32_t)sms;
+    g->C = C;
+    g->P = P;
+    g->hpg = (uint32_t)hpg;
+    g->SB = SB;
+    g->range_log2 = range_log2;
+    g->seg_log2 = seg_log2;
+    g->nseg = (uint32_t)nseg;
+    g->nkeys = nkeys;
+    g->nbuckets = (uint64_t)sms << (range_log2 - vbdr_launch::kSpLineLog2);
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) {
+      const uint64_t o = off;
+      off = align256(off + bytes);
+      return o;
+    };
+    g->off_offs = take(4 * g->nbuckets);
+    g->off_segtot = take(4 * nkeys);
+    g->off_segbase = take(4 * (nkeys + 1));
+    g->off_part = take(C > 1 ? 8ull * sms * hpg : 8);
+    g->off_gcount = take(4ull * P);
+    g->off_misc = take(64);
+    g->off_entries = take(4 * (n_hosts * h->cfg.m + 31 * nkeys));
+    g->bytes = off;
+    return true;
+  }
+  return false;
+}
+
+vbdr_launch::PlanLayout sp_layout(const SpGeom &g, void *d_plan, uint64_t n_hosts) {
+  uint8_t *b = static_cast<uint8_t *>(d_plan);
+  vbdr_launch::PlanLayout pl{};
+  pl.kind = 2;
+  pl.ctas = g.ctas;
+  pl.n_hosts = n_hosts;
+  pl.counts = reinterpret_cast<uint32_t *>(b + g.off_offs);
+  pl.range_size = reinterpret_cast<uint32_t *>(b + g.off_segtot);
+  pl.sp_segbase = reinterpret_cast<uint32_t *>(b + g.off_segbase);
+  pl.sp_part = reinterpret_cast<unsigned long long *>(b + g.off_part);
+  pl.sp_gcount = reinterpret_cast<uint32_t *>(b + g.off_gcount);
+  pl.error = reinterpret_cast<unsigned long long *>(b + g.off_misc);
+  pl.entries = reinterpret_cast<uint32_t *>(b + g.off_entries);
+  pl.sp_C = g.C;
+  pl.sp_hpg = g.hpg;
+  pl.sp_nseg = g.nseg;
+  pl.sp_SB = g.SB;
+  pl.sp_seg_log2 = g.seg_log2;
+  pl.sp_range_log2 = g.range_log2;
+  return pl;
 }
 
 // Pass-id plan (k_estimate.cu) for pools the staged plan cannot take whose
@@ -675,27 +737,62 @@ bool passplan_geom(const vbdr *h, uint64_t n_hosts, PassPlanGeom *g) {
   return true;
 }
 
-vbdr_status vbdr_plan_bytes(const vbdr_t *h, uint64_t n_hosts, uint64_t *bytes) {
-  if (!h || !bytes) return VBDR_EINVAL;
+// Which plan a request gets: internal kind 2 (sorted), 0 (staged) or 1
+// (pass ids), or -1.  VBDR_PLAN_AUTO takes the first that fits in that order.
+int choose_plan(const vbdr *h, uint64_t n_hosts, uint32_t want, PlanGeom *g, PassPlanGeom *pg,
+                SpGeom *sg) {
+  if ((want == VBDR_PLAN_AUTO || want == VBDR_PLAN_SORTED) && sp_geom(h, n_hosts, sg)) return 2;
+  if ((want == VBDR_PLAN_AUTO || want == VBDR_PLAN_STAGED) && plan_geom(h, n_hosts, g)) return 0;
+  if ((want == VBDR_PLAN_AUTO || want == VBDR_PLAN_PASSID) && passplan_geom(h, n_hosts, pg)) return 1;
+  return -1;
+}
+
+vbdr_status vbdr_plan_bytes_kind(const vbdr_t *h, uint64_t n_hosts, uint32_t kind, uint64_t *bytes) {
+  if (!h || !bytes || kind > VBDR_PLAN_SORTED) return VBDR_EINVAL;
   PlanGeom g;
   PassPlanGeom pg;
+  SpGeom sg;
   *bytes = 0;
-  if (plan_geom(h, n_hosts, &g)) {
-    *bytes = g.bytes;
-  } else if (passplan_geom(h, n_hosts, &pg)) {
-    *bytes = pg.bytes;
-  } else {
-    return VBDR_ERANGE;
+  switch (choose_plan(h, n_hosts, kind, &g, &pg, &sg)) {
+    case 2: *bytes = sg.bytes; break;
+    case 0: *bytes = g.bytes; break;
+    case 1: *bytes = pg.bytes; break;
+    default: return VBDR_ERANGE;
   }
   return VBDR_OK;
 }
 
-vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, void *d_plan,
-                            uint64_t bytes, void *stream) {
+vbdr_status vbdr_plan_bytes(const vbdr_t *h, uint64_t n_hosts, uint64_t *bytes) {
+  return vbdr_plan_bytes_kind(h, n_hosts, VBDR_PLAN_AUTO, bytes);
+}
+
+vbdr_status vbdr_plan_build_kind(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts,
+                                 uint32_t kind, void *d_plan, uint64_t bytes, void *stream) {
   if (!h) return VBDR_EINVAL;
+  if (kind > VBDR_PLAN_SORTED) return fail(h, VBDR_EINVAL, "unknown plan kind");
   PlanGeom g;
   PassPlanGeom pg;
-  if (!plan_geom(h, n_hosts, &g) && passplan_geom(h, n_hosts, &pg)) {
+  SpGeom sg;
+  const int which = choose_plan(h, n_hosts, kind, &g, &pg, &sg);
+  if (which < 0) return fail(h, VBDR_ERANGE, "no plan of this kind for this pool / host count");
+  if (which == 2) {
+    if (!d_hosts || !d_plan || (reinterpret_cast<uintptr_t>(d_plan) & 255u))
+      return fail(h, VBDR_EINVAL, "d_hosts and a 256-byte aligned d_plan are required");
+    if (bytes < sg.bytes) return fail(h, VBDR_ENOMEM, "plan buffer too small");
+    if (vbdr_status s = check_async(h, "before plan_build")) return s;
+    cudaStream_t cs = S(stream);
+    const vbdr_launch::PlanLayout pl = sp_layout(sg, d_plan, n_hosts);
+    cudaError_t e = vbdr_launch::sp_build(pl, d_hosts, n_hosts, h->cfg.m, h->p.A0, h->p.mask,
+                                          pl.error, cs);
+    if (e == cudaSuccess)
+      e = vbdr_launch::sp_fill(pl, d_hosts, n_hosts, h->cfg.m, h->p.A0, h->p.mask, cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (e != cudaSuccess) return cuda_fail(h, e, "plan_build");
+    h->info.launches += 5;
+    h->plans[d_plan] = pl;
+    return VBDR_OK;
+  }
+  if (which == 1) {
     if (!d_hosts || !d_plan || (reinterpret_cast<uintptr_t>(d_plan) & 255u))
       return fail(h, VBDR_EINVAL, "d_hosts and a 256-byte aligned d_plan are required");
     if (bytes < pg.bytes) return fail(h, VBDR_ENOMEM, "plan buffer too small");
@@ -718,7 +815,6 @@ vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts
     h->plans[d_plan] = pl;
     return VBDR_OK;
   }
-  if (!plan_geom(h, n_hosts, &g)) return fail(h, VBDR_ERANGE, "no plan for this pool / host count");
   if (!d_hosts || !d_plan || (reinterpret_cast<uintptr_t>(d_plan) & 255u))
     return fail(h, VBDR_EINVAL, "d_hosts and a 256-byte aligned d_plan are required");
   if (bytes < g.bytes) return fail(h, VBDR_ENOMEM, "plan buffer too small");
@@ -741,6 +837,11 @@ vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts
   return VBDR_OK;
 }
 
+vbdr_status vbdr_plan_build(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_hosts, void *d_plan,
+                            uint64_t bytes, void *stream) {
+  return vbdr_plan_build_kind(h, d_hosts, n_hosts, VBDR_PLAN_AUTO, d_plan, bytes, stream);
+}
+
 static vbdr_status estimate_with_plan(vbdr_t *h, const void *d_plan, double *d_out, uint64_t *d_S,
                                       uint32_t *d_V, void *stream) {
   if (!h) return VBDR_EINVAL;
@@ -748,6 +849,14 @@ static vbdr_status estimate_with_plan(vbdr_t *h, const void *d_plan, double *d_o
   if (it == h->plans.end()) return fail(h, VBDR_EINVAL, "unknown plan (build it with this handle)");
   if (vbdr_status s = check_async(h, "before estimate_plan")) return s;
   const vbdr_launch::PlanLayout &pl = it->second;
+  if (pl.kind == 2) {
+    const cudaError_t e = vbdr_launch::estimate_sp(est_params(h), pl, pl.n_hosts, d_out,
+                                                   reinterpret_cast<unsigned long long *>(d_S),
+                                                   d_V, S(stream));
+    if (e != cudaSuccess) return cuda_fail(h, e, "estimate_plan launch");
+    h->info.launches += 1;
+    return VBDR_OK;
+  }
   if (pl.kind == 1) {
     const cudaError_t e = vbdr_launch::estimate_passplan(
         est_params(h), pl.hosts, pl.n_hosts, pl.pid, pl.passes, d_out,
@@ -790,7 +899,7 @@ vbdr_status vbdr_plan_check(vbdr_t *h, const void *d_plan, void *stream) {
   if (!h) return VBDR_EINVAL;
   auto it = h->plans.find(d_plan);
   if (it == h->plans.end()) return fail(h, VBDR_EINVAL, "unknown plan");
-  if (it->second.kind == 1) return VBDR_OK;  // pass ids: nothing is staged
+  if (it->second.kind != 0) return VBDR_OK;  // pass ids / sorted: nothing is staged
   unsigned long long err = 0;
   cudaStream_t cs = S(stream);
   cudaError_t e = cudaMemcpyAsync(&err, it->second.error, 8, cudaMemcpyDeviceToHost, cs);

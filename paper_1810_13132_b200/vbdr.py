@@ -14,9 +14,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# VBDR_LIB points at an alternative build of the same library (kernel-variant
-# experiments in tools/); the default is the in-tree build.
-LIB_PATH = os.environ.get("VBDR_LIB") or os.path.join(_HERE, "_lib", "libvbdr.so")
+LIB_PATH = os.path.join(_HERE, "_lib", "libvbdr.so")  # the in-tree build
 
 LAYOUT_FAST, LAYOUT_PACKED = 0, 1
 LAYOUTS = {"fast": LAYOUT_FAST, "packed": LAYOUT_PACKED}
@@ -50,7 +48,9 @@ SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice",
            "vbdr_slide_peers", "vbdr_plan_bytes", "vbdr_plan_build", "vbdr_estimate_plan",
            "vbdr_host_sums_plan", "vbdr_plan_check", "vbdr_plan_release",
            "vbdr_estimate_plan_host", "vbdr_config_check", "vbdr_select_above",
-           "vbdr_sparse_extract", "vbdr_sparse_apply", "vbdr_last_error", "vbdr_status_string")
+           "vbdr_sparse_extract", "vbdr_sparse_apply", "vbdr_last_error", "vbdr_status_string",
+           "vbdr_plan_bytes_kind", "vbdr_plan_build_kind")
+PLAN_KINDS = {"auto": 0, "staged": 1, "passid": 2, "sorted": 3}
 
 _lib = None
 
@@ -83,6 +83,8 @@ def lib():
             "vbdr_slide_peers": [vp, vp, u32, u64, u64, vp, vp, vp],
             "vbdr_plan_bytes": [vp, u64, C.POINTER(u64)],
             "vbdr_plan_build": [vp, vp, u64, vp, u64, vp],
+            "vbdr_plan_bytes_kind": [vp, u64, u32, C.POINTER(u64)],
+            "vbdr_plan_build_kind": [vp, vp, u64, u32, vp, u64, vp],
             "vbdr_estimate_plan": [vp, vp, vp, vp],
             "vbdr_host_sums_plan": [vp, vp, vp, vp, vp],
             "vbdr_estimate_plan_host": [vp, vp, vp, vp, vp],
@@ -327,25 +329,28 @@ class VBDR:
         return a[order], e[order]
 
     # ---------------------------------------------------- plan-based estimate
-    def plan(self, hosts, stream=None):
-        """``vbdr_plan_bytes`` + ``vbdr_plan_build``: preprocess a fixed host
-        list (device u32/int32 tensor) for repeated estimates -- shared-memory
-        staged rounds for pools up to 2^22 BDRs, pass ids for multi-pass pools
-        (include/vbdr.h).  Returns an :class:`EstimatePlan`; raises ValueError
-        when the pool or host count has no plan (use :meth:`estimate`)."""
+    def plan(self, hosts, kind: str = "auto", stream=None):
+        """``vbdr_plan_bytes_kind`` + ``vbdr_plan_build_kind``: preprocess a
+        fixed host list (device u32/int32 tensor) for repeated estimates --
+        kind "sorted", "staged", "passid" or "auto" (the first that fits, in
+        that order; include/vbdr.h).  Returns an :class:`EstimatePlan`; raises
+        ValueError when the pool or host count has no plan of that kind (use
+        :meth:`estimate`)."""
         import torch
         n = hosts.numel()
+        k = PLAN_KINDS[kind]
         nbytes = C.c_uint64()
-        rc = lib().vbdr_plan_bytes(self._h, n, C.byref(nbytes))
+        rc = lib().vbdr_plan_bytes_kind(self._h, n, k, C.byref(nbytes))
         if rc != 0:
-            raise ValueError(f"no estimate plan for n_phys={self.n_phys}, {n} hosts")
+            raise ValueError(f"no {kind} estimate plan for n_phys={self.n_phys}, {n} hosts")
         buf = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
-        rc = lib().vbdr_plan_build(self._h, C.c_void_p(hosts.data_ptr()), n,
-                                   C.c_void_p(buf.data_ptr()), nbytes.value, _stream_ptr(stream))
-        if rc == -2:  # ERANGE: a block overflows the shared-memory stage
+        rc = lib().vbdr_plan_build_kind(self._h, C.c_void_p(hosts.data_ptr()), n, k,
+                                        C.c_void_p(buf.data_ptr()), nbytes.value,
+                                        _stream_ptr(stream))
+        if rc == -2:  # ERANGE: e.g. a block overflows the shared-memory stage
             raise ValueError(lib().vbdr_last_error(self._h).decode())
-        self._check(rc, "vbdr_plan_build")
-        return EstimatePlan(self, buf, n)
+        self._check(rc, "vbdr_plan_build_kind")
+        return EstimatePlan(self, buf, n, kind)
 
     def estimate_plan(self, plan: "EstimatePlan", out=None, stream=None):
         """``vbdr_estimate_plan``: estimates for the plan's hosts (float64)."""
@@ -449,8 +454,8 @@ class VBDR:
 class EstimatePlan:
     """A host list preprocessed by ``vbdr_plan_build`` (device buffer owned here)."""
 
-    def __init__(self, pool: VBDR, buf, n_hosts: int):
-        self.pool, self.buf, self.n_hosts = pool, buf, n_hosts
+    def __init__(self, pool: VBDR, buf, n_hosts: int, kind: str = "auto"):
+        self.pool, self.buf, self.n_hosts, self.kind = pool, buf, n_hosts, kind
 
     @property
     def nbytes(self) -> int:
@@ -572,13 +577,25 @@ class PeerMerge:
         import torch.distributed as dist
         dist.all_reduce(self.flag, group=self.group)  # stream-ordered across ranks
 
-    def close_slice(self):
+    def peer_regmax_next(self) -> list:
+        """Every rank's register buffer that the next slide writes (it
+        alternates with the tick, which is the same on every rank)."""
+        off = self.pool.info()["off_regmax_next"]
+        return [b + off for b in self.peer_base]
+
+    def close_slice(self, on_merged=None, on_slid=None):
+        """Stamp delta, barrier, fused merge + slide of this rank's shard
+        (writing every rank's registers and sums), barrier.  The optional
+        callbacks run after the first barrier and after the slide launch
+        (bench.py records its phase events there)."""
         self.pool.stamp_delta(self.delta)
         self._barrier()  # every rank's delta is written
-        # the register buffer the slide writes alternates with the tick (same on every rank)
-        off = self.pool.info()["off_regmax_next"]
-        peer_regmax = [b + off for b in self.peer_base]
-        self.pool.slide_peers(self.peer_delta, self.j0, self.j1, peer_regmax, self.peer_acc)
+        if on_merged is not None:
+            on_merged()
+        self.pool.slide_peers(self.peer_delta, self.j0, self.j1, self.peer_regmax_next(),
+                              self.peer_acc)
+        if on_slid is not None:
+            on_slid()
         self._barrier()  # every rank's register shard and sums have landed
 
 

@@ -26,7 +26,7 @@ def test_header_declares_the_boundary():
     names = _declared()
     for n in ("vbdr_create", "vbdr_scan_slice", "vbdr_slide", "vbdr_estimate", "vbdr_destroy"):
         assert n in names
-    assert len(names) == 31
+    assert len(names) == len(set(names)) >= 31
 
 
 def test_library_exports_every_declared_symbol(vb):
@@ -53,9 +53,11 @@ def test_state_bytes_and_validation(vb):
     # layout F: acc 256 B + sr 16 MiB + DRV 3 planes * 16 MiB + two regmax buffers of 4 MiB
     assert vb.state_bytes(cfg) == 256 + 4 * (1 << 22) + 12 * (1 << 22) + 2 * (1 << 22)
     assert vb.state_bytes(vb.make_config(128, 5, 1 << 22)) == vb.state_bytes(cfg)
-    # the binned scan (mode 6) adds 256 bins of 2^23/256 * 9/8 + 512 records + cursors
-    bins = 4 * 256 * (32768 + 4096 + 512) + 4 * 256
-    assert vb.state_bytes(vb.make_config(128, 5, 1 << 22, scan_mode=6)) == vb.state_bytes(cfg) + bins
+    assert vb.state_bytes(vb.make_config(128, 5, 1 << 22, scan_mode=2)) == vb.state_bytes(cfg)
+    # the measured-slower round-1 scan modes are not in the product library
+    for mode in (1, 3, 4, 6, 7):
+        with pytest.raises(ValueError, match="scan_mode"):
+            vb.state_bytes(vb.make_config(128, 5, 1 << 22, scan_mode=mode))
     cfgp = vb.make_config(128, 5, 1 << 22, layout="packed")
     assert vb.state_bytes(cfgp) == 256 + 12 * (1 << 22) + 2 * (1 << 22)
     # bigwin: zb = 6, F = 5, W = 5

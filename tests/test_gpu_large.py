@@ -58,7 +58,7 @@ def expected_ages(per_slice_M, idx, L, zb):
     return ages
 
 
-def run_large(name, m, k, n_phys, n_slices, layout="fast"):
+def run_large(name, m, k, n_phys, n_slices, layout="fast", plan_kinds=("sorted",)):
     tr = synth.CONFIGS[name]
     b = m.bit_length() - 1
     L = 32 - b
@@ -76,28 +76,41 @@ def run_large(name, m, k, n_phys, n_slices, layout="fast"):
         pool.slide()
         per_slice.append(oracle.rebuild(pairs, b, L, n_phys, 0x5EED0001, 0x5EED0002))
         del pairs
-    M = per_slice[0]
-    for x in per_slice[1:]:
+    window = per_slice[-k:]  # W(t-k+1..t): the registers rebuilt from the last k slices
+    M = window[0]
+    for x in window[1:]:
         M = np.maximum(M, x)
     got = pool.export_regmax()
     assert np.array_equal(got, M), "regmax != rebuild from scratch"
     assert pool.export_pool_sums() == oracle_pool_sums(M, L)
     if layout == "fast":
         ages = pool.export_ages_at(sample)
-        assert np.array_equal(ages, expected_ages(per_slice, sample, L, inf["zbits"]))
+        want = expected_ages(per_slice, sample, L, inf["zbits"])
+        assert np.array_equal(ages, want)
+        S_ = (1 << inf["zbits"]) - 1
+        if n_slices > k:  # expired but unsaturated DRs (k <= age < S) were compared
+            assert ((want >= k) & (want < S_)).any()
     S, V = pool.host_sums(dev_u32(hosts))
     Z, Vo = oracle.host_sums_M(M, hosts, b, n_phys)
     assert np.array_equal(V.cpu().numpy().astype(np.uint64), Vo)
     assert np.array_equal(S.cpu().numpy().astype(np.float64) * 2.0 ** -L, Z)
     est = pool.estimate(dev_u32(hosts)).cpu().numpy()
-    try:  # the plan the bench uses for this pool (pass ids for multi-pass pools)
-        plan = pool.plan(dev_u32(hosts))
-    except ValueError:
-        plan = None
-    if plan is not None:
-        assert np.array_equal(pool.estimate_plan(plan).cpu().numpy(), est)
+    for kind in plan_kinds:  # every plan kind this pool takes, on the sampled hosts
+        plan = pool.plan(dev_u32(hosts), kind=kind)
+        assert np.array_equal(pool.estimate_plan(plan).cpu().numpy(), est), kind
         S2, V2 = pool.host_sums_plan(plan)
-        assert torch.equal(S2, S) and torch.equal(V2, V)
+        assert torch.equal(S2, S) and torch.equal(V2, V), kind
+        del plan
+    # the bench's launch configuration: ONE plan (auto) over ALL hosts of the
+    # config, bit-identical to the gather estimate of all hosts; the sampled
+    # hosts are checked against the oracle below
+    all_dev = dev_u32(hosts_all)
+    plan = pool.plan(all_dev)
+    est_all = pool.estimate_plan(plan).cpu().numpy()
+    assert plan.kind == "auto"
+    del plan
+    assert np.array_equal(est_all, pool.estimate(all_dev).cpu().numpy())
+    assert np.array_equal(est_all[hs], est)
     want = oracle.estimate_M(M, hosts, b, n_phys)
     g, z = m, n_phys
     Es = oracle.alpha(g) * g * g / Z
@@ -108,11 +121,13 @@ def run_large(name, m, k, n_phys, n_slices, layout="fast"):
 
 
 def test_10G_full_size():
-    inf = run_large("10G", 256, 10, 1 << 26, 2)
+    """12 slices > k = 10: the sampled DR ages include expired, unsaturated
+    values (k <= age < S = 15) of the Swar<4> instantiation."""
+    inf = run_large("10G", 256, 10, 1 << 26, 12)
     assert inf["zbits"] == 4 and inf["words"] == 3
 
 
 def test_bigwin_full_size_multipass_estimate():
     """2^28 BDRs: the estimate runs in 4 passes over 64 MiB register ranges."""
-    inf = run_large("bigwin", 256, 60, 1 << 28, 3)
+    inf = run_large("bigwin", 256, 60, 1 << 28, 3, plan_kinds=("sorted", "passid"))
     assert inf["zbits"] == 6 and inf["words"] == 5

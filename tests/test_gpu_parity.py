@@ -68,6 +68,11 @@ def compare_boundary(pool, ref: oracle.Pool, refs_other, hosts_np, hosts_dev, wi
             assert np.array_equal(pool.export_ages(), ref.drv()), "DR ages"
         else:
             assert np.array_equal(pool.export_ages(canonical=True), ref.ck()), "C_k"
+            # raw stored values: Alg.8's SlideDR of the next slice already applied
+            # (saturating at S), so ages in [k, S) are checked too, not only C_k
+            S_ = (1 << cfg.zb) - 1
+            assert np.array_equal(pool.export_ages().astype(np.int64),
+                                  np.minimum(ref.drv().astype(np.int64) + 1, S_)), "raw DR ages"
     assert pool.export_pool_sums() == oracle_pool_sums(M, cfg.L)
     if hosts_np is not None:
         S, V = pool.host_sums(hosts_dev)
@@ -81,9 +86,9 @@ def compare_boundary(pool, ref: oracle.Pool, refs_other, hosts_np, hosts_dev, wi
 
 
 @pytest.mark.parametrize("layout", ["fast", "packed"])
-@pytest.mark.parametrize("scan_mode,est_lanes,passes", [(1, 0, 0), (2, 1, 0), (4, 8, 10), (1, 32, 0),
-                                                       (4, 2, 7), (0, 0, 11), (5, 4, 0), (6, 0, 0),
-                                                       (3, 16, 0)])
+@pytest.mark.parametrize("scan_mode,est_lanes,passes", [(2, 0, 0), (2, 1, 0), (5, 8, 10), (2, 32, 0),
+                                                       (5, 2, 7), (0, 0, 11), (5, 4, 0),
+                                                       (0, 16, 0)])
 def test_tiny_every_boundary(layout, scan_mode, est_lanes, passes):
     """configs[0] 'tiny': 10k pairs/slice, 64 hosts, m=32, 2^12 BDRs, k=4."""
     tr = synth.CONFIGS["tiny"]
@@ -111,13 +116,18 @@ def test_tiny_every_boundary(layout, scan_mode, est_lanes, passes):
                          np.concatenate(slices[max(0, t - 3):t + 1]))
 
 
-@pytest.mark.parametrize("scan_mode", [0, 3, 6])
+@pytest.mark.parametrize("scan_mode", [0, 2])
 @pytest.mark.parametrize("layout", ["fast", "packed"])
 @pytest.mark.parametrize("k,m,n_phys", [(1, 2, 64), (3, 16, 1 << 10), (7, 64, 1 << 14),
-                                        (15, 8, 1 << 8), (60, 256, 1 << 16), (300, 4, 1 << 9)])
+                                        (15, 8, 1 << 8), (10, 256, 1 << 16), (60, 256, 1 << 16),
+                                        (300, 4, 1 << 9)])
 def test_configs_sweep_with_empty_slices(layout, k, m, n_phys, scan_mode):
     """Edge cases: k = 1 (discrete window), k = 2^zb - 1, big k (zb up to 9),
-    g < 32 (several hosts per warp), empty slices, tiny pools."""
+    g < 32 (several hosts per warp), empty slices, tiny pools.  Every config
+    runs past k + 5 slices, so DRs sit expired but unsaturated (k <= age < S)
+    -- in particular the 10G (zb = 4, k = 10) and bigwin (zb = 6, k = 60)
+    field widths of the Swar<4> / Swar<6> IsActiveDR instantiations
+    (SlideDR / IsActiveDR; SPEC.md:128 expiry)."""
     b = m.bit_length() - 1
     tr = synth.TraceConfig("sweep", hosts=200, pairs_per_slice=3001, U0=3000, seed=k * 7 + m)
     cfg = oracle.PoolConfig(b=b, k=k, z=n_phys)
@@ -128,7 +138,8 @@ def test_configs_sweep_with_empty_slices(layout, k, m, n_phys, scan_mode):
     assert pool.info()["zbits"] == cfg.zb
     hosts_np = tr.host_ids()
     hosts = dev_u32(hosts_np)
-    n_slices = min(2 * k + 5, 40)
+    n_slices = max(min(2 * k + 5, 40), k + 6)
+    ages_seen = set()
     slices = []
     for t in range(n_slices):
         pairs = synth.generate(tr, t) if t % 4 != 2 else np.zeros((0, 2), np.uint32)
@@ -140,6 +151,10 @@ def test_configs_sweep_with_empty_slices(layout, k, m, n_phys, scan_mode):
         if t % 3 == 0 or t == n_slices - 1:
             compare_boundary(pool, ref, [], hosts_np, hosts,
                              np.concatenate(slices[max(0, t - k + 1):t + 1]))
+            ages_seen |= set(np.unique(ref.drv()).tolist())
+    S = (1 << cfg.zb) - 1
+    if S - 1 >= k:  # the expired-but-unsaturated ages were really exercised
+        assert any(k <= a < S for a in ages_seen), (k, S, sorted(ages_seen))
 
 
 @pytest.mark.parametrize("layout", ["fast", "packed"])
@@ -193,7 +208,7 @@ def test_order_split_and_duplicates_give_identical_state():
 
 
 @pytest.mark.parametrize("layout", ["fast", "packed"])
-@pytest.mark.parametrize("scan_mode", [1, 2, 3, 5, 6])
+@pytest.mark.parametrize("scan_mode", [2, 5])
 def test_bursty_trains_every_scan_mode(layout, scan_mode):
     """Packet trains (consecutive duplicate pairs: whole warps hitting the
     same BDR, the case warp aggregation and the block cache target): state
@@ -286,28 +301,6 @@ def test_register_sharded_state_rules():
     assert (ages[0] == 0).all() and (ages[3] == 0).all()  # outside the shard
 
 
-def test_binned_scan_chunks_and_full_bins():
-    """scan_mode 6 (binned): a call larger than one chunk (several bin + apply
-    rounds) and a skewed batch whose records overflow their bin (the direct
-    atomicMax fallback) leave the same state as the atomic scan (mode 5)."""
-    n_phys = 1 << 16
-    a = VBDR(64, 3, n_phys, device=DEV, scan_mode=6)
-    b = VBDR(64, 3, n_phys, device=DEV, scan_mode=5)
-    assert a.info()["state_bytes"] > b.info()["state_bytes"]  # the bins
-    rng = np.random.default_rng(7)
-    for t in range(5):
-        big = rng.integers(0, 2**32, (300_001, 2), dtype=np.uint64).astype(np.uint32)
-        skew = np.tile(big[:3], (40_000, 1))  # 120k records into <= 3 bins
-        for pairs in (big, skew):
-            a.scan_slice(dev_u32(pairs))
-            b.scan_slice(dev_u32(pairs))
-        a.slide()
-        b.slide()
-        assert np.array_equal(a.export_ages(), b.export_ages())
-        assert np.array_equal(a.export_regmax(), b.export_regmax())
-        assert a.export_pool_sums() == b.export_pool_sums()
-
-
 def test_host_buffer_path_matches_device_path():
     """vbdr_scan_slice_host / vbdr_estimate_host (the end-to-end entry points)."""
     tr = synth.CONFIGS["tiny"]
@@ -332,6 +325,53 @@ def test_host_buffer_path_matches_device_path():
         assert np.array_equal(a.export_ages(), b.export_ages())
 
 
+@pytest.mark.parametrize("name,layout,use_plan", [("caida", "fast", True), ("caida", "packed", True),
+                                                   ("tiny", "fast", False)])
+def test_e2e_pipelined_loop_matches_oracle(name, layout, use_plan):
+    """bench.py's end-to-end loop exactly: vbdr_scan_slice_host through a
+    one-slice staging buffer split in halves (each half's copy overlaps the
+    other half's scan and, across calls, the previous slice's slide and
+    estimate), vbdr_slide, vbdr_estimate_plan_host (or vbdr_estimate_host),
+    and NO synchronisation between steps.  Every slice's host-side estimates,
+    read after one final sync, equal the oracle's at that boundary (PAPER.md:217:
+    only IP pairs are transmitted to the GPU)."""
+    tr = synth.CONFIGS[name]
+    wl = {"tiny": (32, 4, 1 << 12, 5), "caida": (128, 5, 1 << 22, 7)}[name]
+    m, k, z, b = wl
+    cfg = oracle.PoolConfig(b=b, k=k, z=z)
+    ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+    pool = VBDR(m, k, z, layout=layout, device=DEV)
+    hosts_np = tr.host_ids()
+    n_steps = 7
+    slices = [synth.generate(tr, t) for t in range(n_steps)]
+    h_inputs = [torch.from_numpy(p.reshape(-1).view(np.int32)).pin_memory() for p in slices]
+    stage = torch.empty(2 * len(slices[0]), dtype=torch.int32, device=DEV)  # bench: one slice
+    ostage = torch.empty(len(hosts_np), dtype=torch.float64, device=DEV)
+    h_outs = [torch.full((len(hosts_np),), -1.0, dtype=torch.float64).pin_memory()
+              for _ in range(n_steps)]
+    if use_plan:
+        plan = pool.plan(dev_u32(hosts_np))
+    else:
+        h_hosts = torch.from_numpy(hosts_np.view(np.int32)).pin_memory()
+        hstage = torch.empty(len(hosts_np), dtype=torch.int32, device=DEV)
+    torch.cuda.synchronize()
+    for t in range(n_steps):  # no sync inside the loop
+        pool.scan_slice_host(h_inputs[t], stage)
+        pool.slide()
+        if use_plan:
+            pool.estimate_plan_host(plan, ostage, h_outs[t])
+        else:
+            pool.estimate_host(h_hosts, hstage, ostage, h_outs[t])
+    torch.cuda.synchronize()
+    if use_plan:
+        pool.plan_check(plan)
+    for t in range(n_steps):
+        ref.slice(slices[t])
+        M = ref.readout()
+        check_estimates(h_outs[t].numpy(), ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
+    assert np.array_equal(pool.export_regmax(), ref.readout())
+
+
 def test_synth_cuda_twin_matches_numpy():
     for name in ("tiny", "caida", "caida_bursty"):
         tr = synth.CONFIGS[name]
@@ -342,7 +382,7 @@ def test_synth_cuda_twin_matches_numpy():
 
 
 @pytest.mark.parametrize("layout,pass_log2,scan_mode", [("fast", 0, 0), ("packed", 0, 0),
-                                                       ("fast", 20, 6), ("packed", 0, 5)])
+                                                       ("fast", 20, 2), ("packed", 0, 5)])
 def test_caida_full_size(layout, pass_log2, scan_mode):
     """configs[1] 'caida' at full size (5M pairs/slice, 2^22 BDRs, m=128, k=5,
     500k hosts) in the launch configuration bench.py times: every register,
@@ -703,18 +743,19 @@ def test_unusual_configs(layout, m, n_phys, k, zbits, rank_cap):
                      np.concatenate(slices[-k:]))
 
 
+@pytest.mark.parametrize("kind", ["sorted", "staged"])
 @pytest.mark.parametrize("layout,estimator", [("fast", "hll"), ("packed", "hll"),
                                               ("packed", "pcsa"), ("fast", "loglog")])
-def test_plan_estimate_tiny(layout, estimator):
-    """vbdr_estimate_plan: shared-memory-staged sums equal the gather kernel's
-    bit for bit and the oracle to 1e-9, at every boundary."""
+def test_plan_estimate_tiny(layout, estimator, kind):
+    """vbdr_estimate_plan: plan sums equal the gather kernel's bit for bit and
+    the oracle to 1e-9, at every boundary."""
     tr = synth.CONFIGS["tiny"]
     cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
     ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
     pool = VBDR(32, 4, 1 << 12, layout=layout, estimator=estimator, device=DEV)
     hosts_np = tr.host_ids()
     hosts = dev_u32(hosts_np)
-    plan = pool.plan(hosts)
+    plan = pool.plan(hosts, kind=kind)
     for t in range(7):
         pairs = synth.generate(tr, t)
         pool.scan_slice(dev_u32(pairs))
@@ -732,7 +773,8 @@ def test_plan_estimate_tiny(layout, estimator):
     pool.plan_check(plan)
 
 
-def test_plan_estimate_caida_full_size():
+@pytest.mark.parametrize("kind", ["auto", "sorted", "staged"])
+def test_plan_estimate_caida_full_size(kind):
     """configs[1] at full size: the plan covers all 500k hosts of the bench."""
     tr = synth.CONFIGS["caida"]
     cfg = oracle.PoolConfig(b=7, k=5, z=1 << 22)
@@ -740,7 +782,7 @@ def test_plan_estimate_caida_full_size():
     pool = VBDR(128, 5, 1 << 22, device=DEV)
     hosts_np = tr.host_ids()
     hosts = dev_u32(hosts_np)
-    plan = pool.plan(hosts)
+    plan = pool.plan(hosts, kind=kind)
     for t in range(6):
         pairs = synth.generate(tr, t)
         pool.scan_slice(dev_u32(pairs))
@@ -753,9 +795,11 @@ def test_plan_estimate_caida_full_size():
     pool.plan_check(plan)
 
 
+@pytest.mark.parametrize("kind", ["sorted", "staged"])
 @pytest.mark.parametrize("g,z_log2,n_hosts", [(64, 12, 1001), (16, 12, 3),
-                                               (32, 20, 7 * 512 * 148 - 5)])
-def test_plan_accumulator_modes_and_ragged_hosts(g, z_log2, n_hosts):
+                                               (32, 20, 7 * 512 * 148 - 5), (2, 7, 33),
+                                               (256, 24, 300_001)])
+def test_plan_accumulator_modes_and_ragged_hosts(g, z_log2, n_hosts, kind):
     """Plan rounds for a host list with duplicates and a ragged tail, for 3
     hosts (almost every round is padding) and for the largest host count a
     plan takes (20 blocks of 2^16 registers): bit-identical to the gather
@@ -766,7 +810,11 @@ def test_plan_accumulator_modes_and_ragged_hosts(g, z_log2, n_hosts):
     hosts_np = rng.integers(0, 2**32, n_hosts, dtype=np.uint64).astype(np.uint32)
     hosts_np[1::7][:64] = hosts_np[0]  # duplicates (many would pile into a few blocks)
     hosts = dev_u32(hosts_np)
-    plan = pool.plan(hosts)
+    if kind == "staged" and z_log2 > 22:
+        with pytest.raises(ValueError):
+            pool.plan(hosts, kind=kind)
+        return
+    plan = pool.plan(hosts, kind=kind)
     for t in range(6):
         pool.scan_slice(dev_u32(synth.generate(tr, t)))
         pool.slide()
@@ -791,7 +839,7 @@ def test_pass_id_plan_multipass(g, pass_log2):
     hosts_np[5::11] = hosts_np[0]
     hosts_np[:64] = tr.host_ids()  # hosts with traffic
     hosts = dev_u32(hosts_np)
-    plan = pool.plan(hosts)
+    plan = pool.plan(hosts, kind="passid")
     before = pool.info()["launches"]
     for t in range(5):
         pool.scan_slice(dev_u32(synth.generate(tr, t)))
@@ -805,10 +853,19 @@ def test_pass_id_plan_multipass(g, pass_log2):
     pool.plan_check(plan)
 
 
-def test_plan_refuses_large_pools():
+def test_plan_refuses_what_does_not_fit():
+    """staged: pools above 2^22 BDRs; sorted: a group's accumulators beyond the
+    SM's shared memory; auto: neither (and one estimate pass, so no pass ids)."""
     pool = VBDR(256, 10, 1 << 23, device=DEV)
     with pytest.raises(ValueError):
-        pool.plan(dev_u32(np.arange(10, dtype=np.uint32)))
+        pool.plan(dev_u32(np.arange(10, dtype=np.uint32)), kind="staged")
+    many = torch.arange(6_000_000, dtype=torch.int32, device=DEV)
+    with pytest.raises(ValueError):
+        pool.plan(many, kind="sorted")
+    with pytest.raises(ValueError):
+        pool.plan(many)
+    with pytest.raises(KeyError):
+        pool.plan(many, kind="nope")
 
 
 def test_query_top_super_spreaders():
