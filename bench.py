@@ -63,8 +63,11 @@ def parse():
     ap.add_argument("--est-lanes", type=int, default=0)
     ap.add_argument("--est-pass-log2", type=int, default=0)
     ap.add_argument("--estimator", default="hll", choices=["hll", "loglog", "pcsa"])
-    ap.add_argument("--estimate", default="auto", choices=["auto", "gather", "plan"],
-                    help="plan: shared-memory plan for the fixed host list (pools <= 2^22)")
+    ap.add_argument("--estimate", default="auto",
+                    choices=["auto", "gather", "sorted", "staged", "passid"],
+                    help="estimate path: gather (any host list) or a plan built once for the "
+                         "fixed host list (include/vbdr.h vbdr_plan_kind); auto = every path "
+                         "this pool takes, timed on the warm pool, the fastest kept")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo + --same-device: exercise the N>1 control flow on one GPU "
                          "(collectives on the CPU, no GPU-side waiting between ranks)")
@@ -105,16 +108,30 @@ def ceilings():
         return json.load(f)
 
 
-def load_traffic(config: str, layout: str) -> dict:
+def load_traffic(config: str, layout: str, est_path: str) -> dict:
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the last
-    committed ncu --set full capture (profiles/traffic.json), or {}."""
+    committed ncu --set full capture (profiles/traffic.json), or {}.  Keys
+    "<config>/<layout>/<kernel>"; the estimate's key names its path
+    ("estimate/<path>", e.g. "estimate/staged plan")."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
     except Exception:
         return {}
     pre = f"{config}/{layout}/"
-    return {k[len(pre):]: v for k, v in t.items() if k.startswith(pre)}
+    out = {k[len(pre):]: v for k, v in t.items() if k.startswith(pre)}
+    out["estimate"] = out.get(f"estimate/{est_path}")
+    return out
+
+
+def plan_stream_bytes(plan, gathers: int, hosts: int, n_phys: int):
+    """Bytes a plan estimate streams by design: 4 B of plan entry per gather
+    (padding not counted), the register array once, 8 B out per host."""
+    if plan is None:
+        return None
+    if plan.kind == "passid":  # host ids + 2 bits per gather + registers + out
+        return 4 * hosts + gathers // 4 + n_phys + 8 * hosts
+    return 4 * gathers + n_phys + 8 * hosts
 
 
 def table1_bits(m: int, k: int) -> dict:
@@ -356,17 +373,21 @@ def run_vbdr(args):
     hosts_all = tr.host_ids()
     hosts = torch.from_numpy(hosts_all[h0:h1].view(np.int32)).to(dev)
     est_out = torch.empty(h1 - h0, dtype=torch.float64, device=dev)
-    plan, plan_build_ms = None, None
-    if args.estimate in ("auto", "plan"):
+    # plans of every kind this pool takes for the rank's host list (built once,
+    # outside the timed region; the build time is reported)
+    plans, plan_build = {}, {}
+    kinds = ("sorted", "staged", "passid") if args.estimate == "auto" else \
+        (() if args.estimate == "gather" else (args.estimate,))
+    for kind in kinds:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         try:
-            plan = pool.plan(hosts)
-            plan_build_ms = (time.perf_counter() - t0) * 1e3
+            plans[kind] = pool.plan(hosts, kind=kind)
+            plan_build[kind] = round((time.perf_counter() - t0) * 1e3, 2)
         except ValueError:
-            if args.estimate == "plan":
+            if args.estimate != "auto":
                 raise
-            plan = None
+    plan = next(iter(plans.values()), None)
 
     def estimate(out, on=None):
         if plan is not None:
@@ -465,34 +486,43 @@ def run_vbdr(args):
         step(i)
     barrier()
 
-    # --estimate auto: the plan streams the whole register array through every
-    # SM whatever the host count, the gather scales with the hosts; keep the
-    # faster of the two for this rank's host share (same results either way)
+    # --estimate auto: every path this pool takes (the plans of each kind, the
+    # gather) timed on the warm pool; the fastest is kept for this rank's host
+    # share (same results on every path: integer sums, one fp64 finish).  A
+    # staged plan streams the whole register array through every SM whatever
+    # the host count, the gather scales with the hosts, the sorted plan with
+    # both; which wins depends on the pool and the host count.
     est_choice = None
-    if args.estimate == "auto" and plan is not None:
-        def time_est(use_plan):
+    if args.estimate == "auto":
+        def time_est(p):
             evs = [(E(), E()) for _ in range(5)]
             for j in range(7):
                 flush.fill_(j & 0xFF)
                 if j >= 2:
                     evs[j - 2][0].record(stream)
-                if use_plan:
-                    pool.estimate_plan(plan, out=est_out)
+                if p is not None:
+                    pool.estimate_plan(p, out=est_out)
                 else:
                     pool.estimate(hosts, out=est_out)
                 if j >= 2:
                     evs[j - 2][1].record(stream)
             torch.cuda.synchronize()
             return float(np.median([a.elapsed_time(b) for a, b in evs]))
-        t_plan, t_gather = time_est(True), time_est(False)
+        names = ["sorted", "staged", "passid", "gather"]  # same list on every rank
+        times = [time_est(plans.get(n)) if n in plans or n == "gather" else float("inf")
+                 for n in names]
         if world > 1:  # one choice for every rank: the slowest rank decides
-            t = torch.tensor([t_plan, t_gather], dtype=torch.float64, device=dev)
+            t = torch.tensor(times, dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_plan, t_gather = float(t[0]), float(t[1])
-        est_choice = {"plan_ms": round(t_plan, 5), "gather_ms": round(t_gather, 5)}
-        if t_gather < t_plan:
-            plan = None
+            times = t.cpu().tolist()
+        est_choice = {f"{n}_ms": round(t, 5) for n, t in zip(names, times) if t != float("inf")}
+        best = names[int(np.argmin(times))]
+        plan = plans.get(best)
+        for n in list(plans):  # free the plans not kept
+            if n != best:
+                plans.pop(n).release()
         barrier()
+    est_path = "gather" if plan is None else f"{plan.kind} plan"
 
     # ---- device-resident timed region (clocks sampled through it and the e2e region)
     clocks = ClockSampler(gpu) if rank == 0 else None
@@ -523,13 +553,34 @@ def run_vbdr(args):
         return float(sum(per_step)), pool.info()["launches"] - l0, per_step
 
     serial_total, serial_launches, serial_steps = timed_steps(step, args.warmup + args.steps)
-    # headline: the pipelined steady state (same work per step)
-    staged_plan = plan is not None and wl["n_phys"] <= (1 << 22)
-    pipelined = args.pipeline == "on" or (args.pipeline == "auto" and staged_plan)
+    # the pipelined schedule (same work per step: one scan, one slide, one
+    # estimate); --pipeline auto times both and the faster is the headline
+    pipe = None
+    if args.pipeline in ("on", "auto"):
+        pipe = timed_steps(step_pipelined, args.warmup + 2 * args.steps)
+        if world > 1:  # one choice on every rank
+            t = torch.tensor([serial_total, pipe[0]], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            st, pt = float(t[0]), float(t[1])
+        else:
+            st, pt = serial_total, pipe[0]
+    pipelined = pipe is not None and (args.pipeline == "on" or pt < st)
     if pipelined:
-        local_total, launches, local_steps = timed_steps(step_pipelined, args.warmup + 2 * args.steps)
+        local_total, launches, local_steps = pipe
     else:
         local_total, launches, local_steps = serial_total, serial_launches, serial_steps
+    pipelined_ms = pipe[0] / args.steps if pipe is not None else None
+    # the step with the gather estimate (any host list, no plan): serial
+    gather_ms = None
+    if plan is not None:
+        kept = plan
+        plan = None
+        gather_ms = timed_steps(step, args.warmup + 3 * args.steps)[0] / args.steps
+        plan = kept
+        if world > 1:
+            t = torch.tensor([gather_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            gather_ms = float(t[0])
     # per-step spread (median and min over the measured slices)
     step_stats = np.array([np.median(local_steps), np.min(local_steps), np.max(local_steps)])
     if world > 1:
@@ -608,60 +659,48 @@ def run_vbdr(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of each kernel; the dominant one goes in "roofline"
+    # ---- roofline of each kernel; the dominant one goes in "roofline".
+    # achieved = SURVEY 8(d.4) algorithmic work per launch / the kernel's mean
+    # CUDA-event time in the breakdown pass (DESIGN.md section 6 states each).
     hbm, hbm_src = peaks()
     ceil = ceilings()
     names = ["scan", "merge", "slide", "estimate"]
     kern = {n: float(v) for n, v in zip(names, per_kernel)}
-    traffic = load_traffic(args.config, args.layout)
+    traffic = load_traffic(args.config, args.layout, est_path)
     slide_bytes = algorithmic_bytes_per_bdr(args.layout, info["words"]) * wl["n_phys"]
     slide_gbs = slide_bytes / (kern["slide"] * 1e-3) / 1e9
-    # the estimate gathers from at most 2^26 registers per pass (64 MiB, L2-resident)
-    regmax_mib = min(wl["n_phys"], 1 << 26) >> 20
-    tab = "4MiB" if regmax_mib <= 4 else "64MiB"
-    sr_mib = 4 * wl["n_phys"] >> 20
-    red_tab = "16MiB" if sr_mib <= 16 else "48MiB" if sr_mib <= 48 else "256MiB" \
-        if sr_mib <= 256 else "1024MiB"
-    gathers = (h1 - h0) * wl["m"]
+    n_hosts = h1 - h0
+    gathers = n_hosts * wl["m"]
+    # estimate, per host: 4 B host id in + 8 B estimate out + g one-byte registers
+    est_bytes = n_hosts * (4 + 8 + wl["m"])
+    est_gbs = est_bytes / (kern["estimate"] * 1e-3) / 1e9
     g_rate = gathers / (kern["estimate"] * 1e-3) / 1e9
     scan_rate = n_local / (kern["scan"] * 1e-3) / 1e9
+    req_peak = ceil["ldg_gather_1B_Gps"]["4MiB"]
     kernels = {
-        "scan": {"ms": kern["scan"], "bound": "l2_atomic", "achieved": round(scan_rate, 2),
-                 "peak": ceil["red_max_u32_Gps"][red_tab], "unit": "Gpairs/s",
-                 "frac": round(scan_rate / ceil["red_max_u32_Gps"][red_tab], 4),
+        "scan": {"ms": kern["scan"], "bound": "l2_requests", "achieved": round(scan_rate, 2),
+                 "peak": req_peak, "unit": "Gpairs/s", "frac": round(scan_rate / req_peak, 4),
                  "traffic": traffic.get("scan"),
-                 "peak_source": f"random atomicMax ceiling, {red_tab} array ({CEIL_SRC})"},
+                 "peak_source": "SM-to-L2 request rate: random 1-byte loads from an "
+                                f"L2-resident table ({CEIL_SRC}); every pair costs at least "
+                                "one L2 request (its check load or its atomic) unless the "
+                                "block's shared-memory cache absorbs it"},
         "merge": {"ms": kern["merge"]},
         "slide": {"ms": kern["slide"], "bound": "hbm", "achieved": round(slide_gbs, 1),
                   "peak": hbm, "unit": "GB/s", "frac": round(slide_gbs / hbm, 4),
                   "traffic": traffic.get("slide"), "algorithmic_bytes": slide_bytes,
                   "peak_source": hbm_src},
-        "estimate": {"ms": kern["estimate"], "bound": "l2_gather", "achieved": round(g_rate, 2),
-                     "peak": ceil["ldg_gather_1B_Gps"][tab], "unit": "Ggathers/s",
-                     "frac": round(g_rate / ceil["ldg_gather_1B_Gps"][tab], 4),
-                     "traffic": traffic.get("estimate"), "hosts": h1 - h0, "gathers": gathers,
-                     "peak_source": f"random 1-byte LDG gather ceiling, {tab} table ({CEIL_SRC})"},
+        "estimate": {"ms": kern["estimate"], "path": est_path, "bound": "hbm",
+                     "achieved": round(est_gbs, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(est_gbs / hbm, 4), "algorithmic_bytes": est_bytes,
+                     "traffic": traffic.get("estimate"),
+                     "traffic_impl": plan_stream_bytes(plan, gathers, n_hosts, wl["n_phys"]),
+                     "hosts": n_hosts, "gathers": gathers, "gathers_per_s": round(g_rate * 1e9),
+                     "peak_source": hbm_src,
+                     "note": "algorithmic bytes = SURVEY 8(d.4): 4 B host in + 8 B out + g x "
+                             "1 B registers per host; traffic_impl = what the path streams "
+                             "by design (plan entries, 4 B per gather)"},
     }
-    staged = plan is not None and wl["n_phys"] <= (1 << 22)  # else a pass-id plan
-    if plan is not None and not staged:
-        kernels["estimate"]["path"] = "pass-id plan (gathers of this pass's registers only)"
-    if staged:
-        # The plan path streams, per slice: 4 B of plan entry per gather, the
-        # round starts, the register array once per SM (from L2; counted once
-        # here as DRAM bytes), 8 B of estimate per host.
-        ctas = torch.cuda.get_device_properties(dev).multi_processor_count
-        phases = max(1, wl["n_phys"] >> 16)
-        plan_bytes = 4 * gathers + 4 * ctas * phases * 20 + wl["n_phys"] + 8 * (h1 - h0)
-        plan_gbs = plan_bytes / (kern["estimate"] * 1e-3) / 1e9
-        kernels["estimate"] = {
-            "ms": kern["estimate"], "path": "plan", "bound": "hbm", "achieved": round(plan_gbs, 1),
-            "peak": hbm, "unit": "GB/s", "frac": round(plan_gbs / hbm, 4),
-            "algorithmic_bytes": plan_bytes, "traffic": traffic.get("estimate_plan"),
-            "gathers_per_s": round(g_rate * 1e9), "hosts": h1 - h0, "gathers": gathers,
-            "peak_source": hbm_src,
-            "note": "HBM is not what binds it: the two-stage TMA block pipeline does "
-                    "(block streaming without compute takes ~85 % of its time; "
-                    "profiles/r01_plan_variants.txt)"}
     dominant = max(("scan", "slide", "estimate"), key=lambda n: kern[n])
     roof = {"kernel": dominant, **{k: v for k, v in kernels[dominant].items() if k != "ms"}}
 
@@ -676,6 +715,8 @@ def run_vbdr(args):
         "value": round(value, 3), "unit": "Mpairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
         "ms_per_step_serial": round(serial_ms, 5),
+        # the same step with the gather estimate (an arbitrary host list, no plan)
+        "ms_per_step_gather": round(gather_ms, 5) if gather_ms is not None else round(serial_ms, 5),
         "step_ms": {"median": round(float(step_stats[0]), 5), "min": round(float(step_stats[1]), 5),
                     "max": round(float(step_stats[2]), 5)},
         "higher_is_better": True,
@@ -689,12 +730,11 @@ def run_vbdr(args):
                    "schedule": ("pipelined: estimate(t) on a 2nd stream overlaps scan(t+1) "
                                 "and slide(t+1)"
                                 if pipelined else "serial"),
+                   "ms_per_step_pipelined": round(pipelined_ms, 5) if pipelined_ms else None,
                    "scan_mode": args.scan_mode, "est_lanes": args.est_lanes,
                    "estimator": args.estimator,
-                   "estimate_path": ("gather" if plan is None else
-                                     "plan (shared-memory staged)" if staged else
-                                     "plan (pass ids, multi-pass gather)"),
-                   "plan_build_ms": round(plan_build_ms, 2) if plan_build_ms else None,
+                   "estimate_path": est_path,
+                   "plan_build_ms": plan_build.get(plan.kind) if plan is not None else None,
                    "estimate_autotune": est_choice,
                    "plan_bytes": plan.nbytes if plan is not None else None,
                    "zbits": info["zbits"], "words_per_bdr": info["words"],

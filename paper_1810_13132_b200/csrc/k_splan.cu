@@ -249,38 +249,70 @@ k_estimate_sp(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out,
   const uint32_t K = 1u << e.L;  // HLL: 2^(L - M) = K >> M
   const uint32_t sacc = (uint32_t)__cvta_generic_to_shared(Sacc);
   const uint32_t vacc = (uint32_t)__cvta_generic_to_shared(Vacc);
+  // the warp's current segment: its end (in rounds) and its register base,
+  // kept in registers; crossing into the next segment is a rare warp-uniform
+  // branch (segments hold whole rounds)
   uint32_t s = 0;
   while (s + 1 < nseg && rs[s + 1] <= r0) ++s;
+  uint32_t seg_end = rs[s + 1];
+  const uint8_t *rb = reg + ((uint64_t)s << segl);
+  auto seg_at = [&](uint32_t rr) {
+    if (rr >= seg_end) {
+      do {
+        ++s;
+        seg_end = rs[s + 1];
+      } while (rr >= seg_end);
+      rb = reg + ((uint64_t)s << segl);
+    }
+  };
+  // one entry: 2^(L - M) (HLL; M for LogLog / PCSA) into S'[slot] if M >= 1,
+  // else 1 into V[slot] -- one shared-memory atomic, address and value selected
   auto add = [&](uint32_t v, uint32_t M) {
     const uint32_t slot = v & smask;
-    uint32_t addr, val;
-    if (M != 0u) {
-      addr = sacc + 4u * slot;
-      val = HLL ? K >> M : M;
-    } else {
-      addr = vacc + 4u * slot;
-      val = 1u;
-    }
+    const bool zero = M == 0u;
+    const uint32_t addr = (zero ? vacc : sacc) + 4u * slot;
+    const uint32_t val = zero ? 1u : (HLL ? K >> M : M);
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(val) : "memory");
   };
   constexpr int U = vbdr_launch::kSpUnroll;
   uint32_t r = r0;
-  for (; r + U <= r1; r += U) {
-    uint32_t v[U], M[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = __ldcs(ent + 32u * (r + u));
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      while (r + u >= rs[s + 1]) ++s;  // warp-uniform: segments hold whole rounds
-      M[u] = __ldg(reg + ((uint64_t)s << segl) + (v[u] >> SB));
+  const uint32_t *ep = ent + 32ull * r0;  // this lane's entry of round r
+  for (; r + U <= r1; r += U, ep += 32 * U) {
+#if VBDR_SP_PREFETCH
+    // pull the warp's entries VBDR_SP_PREFETCH rounds ahead into L2 (one
+    // bulk prefetch per 16 rounds = 2 KB), so the loads below wait on L2
+    if (lane == 0 && ((r - r0) & 15u) < (uint32_t)U) {
+      const uint32_t a = r + VBDR_SP_PREFETCH;
+      if (a < r1) {
+        const uint32_t nb = (min(a + 16u, r1) - a) * 128u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ep + 32u * VBDR_SP_PREFETCH),
+                     "r"(nb) : "memory");
+      }
     }
+#endif
+    uint32_t v[U], M[U];
+    const uint8_t *pa[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(ep + 32 * u);  // streamed once
+    if (r + U <= seg_end) {  // the whole batch in the current segment (usual)
+#pragma unroll
+      for (int u = 0; u < U; ++u) pa[u] = rb + (v[u] >> SB);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        seg_at(r + u);
+        pa[u] = rb + (v[u] >> SB);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) M[u] = __ldg(pa[u]);  // neighbouring registers: L1 hits
 #pragma unroll
     for (int u = 0; u < U; ++u) add(v[u], M[u]);
   }
-  for (; r < r1; ++r) {
-    const uint32_t v = __ldcs(ent + 32u * r);
-    while (r >= rs[s + 1]) ++s;
-    add(v, __ldg(reg + ((uint64_t)s << segl) + (v >> SB)));
+  for (; r < r1; ++r, ep += 32) {
+    const uint32_t v = __ldcs(ep);
+    seg_at(r);
+    add(v, __ldg(rb + (v >> SB)));
   }
   __syncthreads();
   pdl_trigger();

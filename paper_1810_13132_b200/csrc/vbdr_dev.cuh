@@ -194,9 +194,12 @@ constexpr int kPlanStride = 20;   // round starts per (CTA, block): 16 warps + t
 constexpr int kSpThreads = 1024;
 constexpr uint32_t kSpLineLog2 = 7;  // bucket = one 128-byte line of registers
 #ifndef VBDR_SP_UNROLL
-#define VBDR_SP_UNROLL 4
+#define VBDR_SP_UNROLL 8
 #endif
 constexpr int kSpUnroll = VBDR_SP_UNROLL;
+#ifndef VBDR_SP_PREFETCH
+#define VBDR_SP_PREFETCH 64 // rounds ahead to bulk-prefetch into L2 (0 = off)
+#endif
 struct PlanLayout {
   uint32_t kind;         // 0: shared-memory staged rounds (k_plan.cu); 1: pass ids; 2: sorted (k_splan.cu)
   uint32_t ctas, phases, block_log2;

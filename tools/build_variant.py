@@ -1,5 +1,5 @@
-"""Build libvbdr.so variants with extra nvcc defines into tools/variants/<name>/
-(for kernel A/B experiments: VBDR_LIB=tools/variants/<name>/libvbdr.so)."""
+"""Build libvbdr.so variants with extra nvcc defines into tools/var_build/<name>/
+(for kernel A/B experiments: VBDR_LIB=tools/var_build/<name>/libvbdr.so)."""
 import os
 import subprocess
 import sys
@@ -10,7 +10,7 @@ from paper_1810_13132_b200 import _build  # noqa: E402
 
 
 def build(name, defines):
-    out = os.path.join(ROOT, "tools", "variants", name)
+    out = os.path.join(ROOT, "tools", "var_build", name)
     os.makedirs(out, exist_ok=True)
     objs = []
     for src, extra in _build.SOURCES:
