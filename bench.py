@@ -77,7 +77,7 @@ def parse():
                     help="N>1 with --merge sharded/sparse: each rank stores only its "
                          "shard's DRV (register-sharded state, DRV memory /N)")
     ap.add_argument("--merge", default="sharded",
-                    choices=["stamps", "delta", "sharded", "sparse", "p2p"],
+                    choices=["stamps", "delta", "sharded", "sparse", "p2p", "nvls"],
                     help="N>1 slide merge (paper_1810_13132_b200.slide_merged)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--pipeline", default="auto", choices=["auto", "on", "off"],
@@ -323,9 +323,9 @@ def run_vbdr(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1810_13132_b200 import (VBDR, PeerMerge, all_gather_shards, make_config,
-                                       merge_stamps, reduce_scatter_max, shard_range,
-                                       slide_merged)
+    from paper_1810_13132_b200 import (VBDR, NvlsMerge, PeerMerge, SparseMerge,
+                                       all_gather_shards, make_config, merge_stamps,
+                                       reduce_scatter_max, shard_range)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -348,17 +348,43 @@ def run_vbdr(args):
 
     tr = synth.CONFIGS[args.config]
     wl = WORKLOADS[args.config]
-    if world > 1 and args.layout != "fast":
-        raise SystemExit("multi-GPU needs --layout fast (NCCL has no bitwise-AND merge for packed)")
-    state = None
-    if world > 1 and args.merge == "p2p":  # pool state in symmetric memory (peer-writable)
-        state = PeerMerge.alloc_state(make_config(wl["m"], wl["k"], wl["n_phys"]), dev)
-    shard_state = args.shard_state and world > 1 and args.merge in ("sharded", "sparse")
+    if world > 1 and args.layout != "fast" and args.merge != "nvls":
+        raise SystemExit("multi-GPU layout packed needs --merge nvls (NCCL has no bitwise-AND "
+                         "reduction; the NVSwitch multimem.ld_reduce has)")
+    if world > 1:
+        print(f"rank {rank}: {args.dist_backend} communicator of {dist.get_world_size()} ranks, "
+              f"device {torch.cuda.get_device_name(dev)} (cuda:{gpu})", file=sys.stderr, flush=True)
+    shard_state = args.shard_state and world > 1 and args.merge in ("sharded", "sparse", "nvls") \
+        and args.layout == "fast"
+    state, mcbuf, mc_note = None, None, None
+    one_nvls = world == 1 and args.merge == "nvls"
+    if one_nvls:
+        # one GPU: the multicast slide on a one-device multicast object (the
+        # kernel's cost without peers; McBuffer = vbdr_mc_alloc), or, where
+        # the driver refuses multicast objects, the group-of-one form of the
+        # same kernel through the pool's own state
+        from paper_1810_13132_b200 import McBuffer, state_bytes
+        try:
+            mcbuf = McBuffer(state_bytes(make_config(wl["m"], wl["k"], wl["n_phys"],
+                                                     layout=args.layout)), dev)
+            state = mcbuf.tensor
+            mc_note = "slide through a one-device multicast object (NVLS kernel)"
+        except RuntimeError as e:
+            mc_note = (f"multicast slide kernel, group of one through the pool's own state "
+                       f"(no multicast object here: {str(e)[:120]})")
+    if world > 1 and args.merge in ("p2p", "nvls"):  # pool state in symmetric memory
+        cfg = make_config(wl["m"], wl["k"], wl["n_phys"], layout=args.layout,
+                          drv_shards=world if shard_state else 0,
+                          drv_shard=rank if shard_state else 0)
+        state = PeerMerge.alloc_state(cfg, dev)
     pool = VBDR(wl["m"], wl["k"], wl["n_phys"], layout=args.layout, scan_mode=args.scan_mode,
                 est_lanes=args.est_lanes, est_pass_log2=args.est_pass_log2,
                 estimator=args.estimator, device=dev, state=state,
                 drv_shards=world if shard_state else 0, drv_shard=rank if shard_state else 0)
-    peer = PeerMerge(pool, group) if state is not None else None
+    peer = None
+    if state is not None and world > 1:
+        peer = PeerMerge(pool, group) if args.merge == "p2p" else NvlsMerge(pool, group)
+    sparse = SparseMerge(pool, group) if world > 1 and args.merge == "sparse" else None
     info = pool.info()
     p0, p1 = shard_range(tr.pairs_per_slice, rank, world)
     h0, h1 = shard_range(tr.hosts, rank, world)
@@ -421,17 +447,20 @@ def run_vbdr(args):
         [merge] -> slide kernel -> [register all-gather + pool-sum all-reduce]."""
         if world == 1:
             mark(evs, 2)
-            pool.slide()
+            if one_nvls:
+                pool.slide_multicast(mcbuf.mc if mcbuf is not None else pool.state.data_ptr())
+            else:
+                pool.slide()
             mark(evs, 3)
         elif args.merge == "stamps":
             merge_stamps(pool, group)
             mark(evs, 2)
             pool.slide()
             mark(evs, 3)
-        elif args.merge == "p2p":
+        elif args.merge in ("p2p", "nvls"):
             peer.close_slice(on_merged=lambda: mark(evs, 2), on_slid=lambda: mark(evs, 3))
         elif args.merge == "sparse":
-            slide_merged(pool, group, "sparse", shard=shard_buf)
+            sparse.close_slice()
             mark(evs, 2)
             mark(evs, 3)
         elif args.merge == "delta":
@@ -654,6 +683,8 @@ def run_vbdr(args):
         pool.plan_check(plan)  # raises (non-zero exit) if any timed estimate failed
     if bool(torch.isnan(est_out).any()):
         raise SystemExit("bench: NaN estimates (a failed plan estimate)")
+    if sparse is not None:
+        sparse.check()  # raises if a fixed-capacity record buffer ever overflowed
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -725,7 +756,8 @@ def run_vbdr(args):
                    "pairs_per_slice": tr.pairs_per_slice, "hosts": tr.hosts,
                    "parallelism": (f"pairs+hosts sharded x{world}, merge={args.merge}"
                                    + (", register-sharded state" if shard_state else "")
-                                   if world > 1 else "single GPU"),
+                                   if world > 1 else "single GPU" +
+                                   (f", {mc_note}" if mc_note else "")),
                    "l2": f"flushed before every step ({args.flush_mib} MiB write)",
                    "schedule": ("pipelined: estimate(t) on a 2nd stream overlaps scan(t+1) "
                                 "and slide(t+1)"

@@ -230,6 +230,44 @@ vbdr_status vbdr_slide_peers(vbdr_t *h, const uint8_t *const *h_peer_delta, uint
                              uint64_t j0, uint64_t j1, uint8_t *const *h_peer_regmax,
                              uint64_t *const *h_peer_acc, void *stream);
 
+/* Fused NVLS merge + slide, both layouts.  d_mc_state is
+ * the MULTICAST address of a multicast object to which every rank bound its
+ * state buffer (each laid out by vbdr_create with the same config; e.g. torch
+ * symmetric memory's multicast_ptr, or vbdr_mc_alloc for one device).  The
+ * kernel closes the slice for BDRs [j0, j1) (multiples of 4; the rank's
+ * shard) with the merge done by the NVSwitch as it loads:
+ *  - layout fast: multimem.ld_reduce MAX of every rank's stamp words -- the
+ *    serial max of Alg.4 is commutative and idempotent, so the
+ *    reduced stamp is the whole slice's nowLBP1 -- then Alg.1 and Alg.2 on
+ *    the local DRV shard ([j0, j1) must lie in this handle's DRV shard);
+ *  - layout packed: multimem.ld_reduce AND of every rank's copy of the DRV
+ *    words -- each rank's scan cleared fields of its own copy (Alg.9 SetDR,
+ *    PAPER.md:292; clears commute), so the AND holds every
+ *    clear of the slice -- then Alg.2 and Alg.8, and the new words are
+ *    stored into every rank's copy (multimem.st); needs drv_shards <= 1.
+ * The registers of [j0, j1) are stored into every rank's register buffer
+ * (multimem.st) and the shard's pool sums added into every rank's
+ * accumulator (multimem.red).  The caller orders it between two cross-rank
+ * barriers: after every rank's scan of the slice, and before any rank's next
+ * scan or estimate.  Closes the slice like vbdr_slide.  d_mc_state may also be
+ * this handle's own d_state: a group of one with no multicast object, where
+ * the same kernel runs with the multimem operations replaced by the ordinary
+ * load, store and atomic they reduce to over a single member (tests; one
+ * GPU whose driver cannot create multicast objects). */
+vbdr_status vbdr_slide_multicast(vbdr_t *h, void *d_mc_state, uint64_t j0, uint64_t j1,
+                                 void *stream);
+
+/* SYNC.  Test / single-GPU support for vbdr_slide_multicast: allocate
+ * >= bytes of device memory on the current device bound to a one-device
+ * multicast object; *d_uc receives the ordinary (unicast) address to pass to
+ * vbdr_create, *d_mc the multicast address of the same memory, *granted the
+ * size (rounded up to the multicast granularity).  VBDR_ECUDA if the device or
+ * driver has no multicast support.  Free with vbdr_mc_free(d_uc). */
+vbdr_status vbdr_mc_alloc(uint64_t bytes, void **d_uc, void **d_mc, uint64_t *granted);
+vbdr_status vbdr_mc_free(void *d_uc);
+/* Why the calling thread's last vbdr_mc_alloc failed ("" after a success). */
+const char *vbdr_mc_last_error(void);
+
 /* Estimate |OP(aip, t, k)| (Definition 1) for n_hosts hosts
  * over the window W(t-k+1..t) of the last closed slice: Alg.5 gather
  * (PAPER.md:197-213), HyperLogLog harmonic mean with linear counting, vHLL

@@ -33,6 +33,7 @@ SOURCES = [
     ("k_plan.cu", ["-fmad=false"]),
     ("k_splan.cu", ["-fmad=false"]),
     ("vbdr_host.cu", []),
+    ("vbdr_mc.cu", []),
 ]
 
 

@@ -170,7 +170,58 @@ k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict
 //               peer register/accumulator pointers the kernel also writes its
 //               register shard and adds its pool sums into every rank.
 // Only BDR quads [q0, q1) are processed (the rank's shard).
-enum { SRC_STAMPS = 0, SRC_DELTA = 1, SRC_PEERS = 2 };
+//   SRC_NVLS:   every rank's copy of the state in one multicast (NVLS) object
+//               (vbdr_slide_multicast): the merge is done by
+//               the NVSwitch as the kernel loads -- multimem.ld_reduce MAX of
+//               the stamps (layout fast) or AND of the packed DRV words
+//               (layout packed: every rank cleared fields of its own copy,
+//               Alg.9 SetDR, and AND merges clears) -- and the kernel's results
+//               go to every rank with multimem.st (registers; packed: the new
+//               DRV words) and multimem.red (pool sums).  No collective runs.
+//   SRC_ONE:    SRC_NVLS for a group of one without a multicast object (the
+//               "multicast" address is the handle's own state): the same
+//               kernel with the multimem operations replaced by the ordinary
+//               load / store / atomic they reduce to over a single member.
+enum { SRC_STAMPS = 0, SRC_DELTA = 1, SRC_PEERS = 2, SRC_NVLS = 3, SRC_ONE = 4 };
+
+template <bool MC>
+__device__ __forceinline__ uint32_t mc_ld_max(const uint32_t *a) {
+  if constexpr (!MC) return __ldcg(a);
+  uint32_t v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.max.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+template <bool MC>
+__device__ __forceinline__ unsigned long long mc_ld_and64(const uint32_t *a) {
+  if constexpr (!MC) return __ldcg(reinterpret_cast<const unsigned long long *>(a));
+  unsigned long long v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.and.b64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+template <bool MC>
+__device__ __forceinline__ void mc_st64(uint32_t *a, unsigned long long v) {
+  if constexpr (!MC) {
+    __stcg(reinterpret_cast<unsigned long long *>(a), v);
+    return;
+  }
+  asm volatile("multimem.st.relaxed.sys.global.b64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+template <bool MC>
+__device__ __forceinline__ void mc_st32(void *a, uint32_t v) {
+  if constexpr (!MC) {
+    __stcg(reinterpret_cast<uint32_t *>(a), v);
+    return;
+  }
+  asm volatile("multimem.st.relaxed.sys.global.b32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+template <bool MC>
+__device__ __forceinline__ void mc_red_add64(unsigned long long *a, unsigned long long v) {
+  if constexpr (!MC) {
+    atomicAdd(a, v);
+    return;
+  }
+  asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
 
 // PCSA (layout packed only): the register value written is R = the number of
 // consecutive active ranks from rank 1 (the sliding FM bitmap's lowest zero,
@@ -182,6 +233,8 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
   pdl_wait();
   using S = Swar<ZB>;
   constexpr int WM = WMax<ZB>::value;
+  constexpr bool NV = SRC == SRC_NVLS || SRC == SRC_ONE;  // the multicast slide
+  constexpr bool MC = SRC == SRC_NVLS;                    // ... through real multimem ops
   const uint4 *sr4 = reinterpret_cast<const uint4 *>(p.sr);
   // the DRV holds BDR quads [dq0, dq0 + dn4) (all of them unless register-sharded)
   const uint64_t dn4 = p.drv_n >> 2, dq0 = p.drv_j0 >> 2;
@@ -202,6 +255,12 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
         d = __vmaxu4(d, __ldcs(reinterpret_cast<const uint32_t *>(peers.delta[r]) + q));
 #pragma unroll
       for (int c = 0; c < 4; ++c) hit[c] = (d >> (8 * c)) & 0xFFu;
+    } else if constexpr (FAST && NV) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {  // max over every rank's stamp (NVSwitch reduction)
+        const uint32_t sv = mc_ld_max<MC>(peers.sr_mc + 4 * q + c);
+        hit[c] = ((sv >> 5) == p.tick) ? (sv & 31u) : 0u;
+      }
     } else if constexpr (FAST) {
       const uint4 s = __ldcs(sr4 + q);
       const uint32_t sv[4] = {s.x, s.y, s.z, s.w};
@@ -210,8 +269,26 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
     }
     uint4 x[WM];
 #pragma unroll
-    for (int w = 0; w < WM; ++w)
-      if (w < (int)p.W) x[w] = drv4[(uint64_t)w * dn4 + (q - dq0)];
+    for (int w = 0; w < WM; ++w) {
+      if (w >= (int)p.W) continue;
+      if constexpr (!FAST && NV) {  // AND over every rank's copy of the words
+        const uint32_t *a = peers.drv_mc + (uint64_t)w * p.drv_n + 4 * q;
+        const unsigned long long lo = mc_ld_and64<MC>(a), hi = mc_ld_and64<MC>(a + 2);
+        x[w] = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+      } else {
+        x[w] = drv4[(uint64_t)w * dn4 + (q - dq0)];
+      }
+    }
+    // where the slid words go: local, or (packed, NVLS) every rank's copy
+    auto store_words = [&](int w, const uint4 &v) {
+      if constexpr (!FAST && NV) {
+        uint32_t *a = peers.drv_mc + (uint64_t)w * p.drv_n + 4 * q;
+        mc_st64<MC>(a, (unsigned long long)v.x | ((unsigned long long)v.y << 32));
+        mc_st64<MC>(a + 2, (unsigned long long)v.z | ((unsigned long long)v.w << 32));
+      } else {
+        drv4[(uint64_t)w * dn4 + (q - dq0)] = v;
+      }
+    };
     uint32_t best[4] = {0u, 0u, 0u, 0u};
     uint32_t run[4] = {0u, 0u, 0u, 0u};  // PCSA: active ranks from the bottom of word w up
 #pragma unroll
@@ -236,7 +313,7 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
       // warp (typical for the high-rank words) skip the SWAR work.
       if (__all_sync(__activemask(), sat)) {
 #if VBDR_SLIDE_SKIP == 2
-        drv4[(uint64_t)w * dn4 + (q - dq0)] = x[w];  // unchanged, stored anyway
+        store_words(w, x[w]);  // unchanged, stored anyway
 #endif
         if constexpr (PCSA) {
 #pragma unroll
@@ -261,14 +338,16 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
           run[c] = inact ? (uint32_t)(__ffs(inact) - 1) / (uint32_t)ZB : (uint32_t)S::F + run[c];
         }
       }
-      drv4[(uint64_t)w * dn4 + (q - dq0)] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
+      store_words(w, make_uint4(xv[0], xv[1], xv[2], xv[3]));
     }
     if constexpr (PCSA) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) best[c] = min(run[c], p.L);
     }
     const uint32_t r4 = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
-    if (SRC == SRC_PEERS && peers.n_regmax > 0) {
+    if constexpr (NV) {
+      mc_st32<MC>(peers.regmax_mc + 4 * q, r4);  // every rank's register buffer
+    } else if (SRC == SRC_PEERS && peers.n_regmax > 0) {
       for (uint32_t r = 0; r < peers.n_regmax; ++r) reinterpret_cast<uint32_t *>(peers.regmax[r])[q] = r4;
     } else {
       reg4[q] = r4;
@@ -302,7 +381,10 @@ k_slide(DevParams p, uint32_t addk, uint32_t slot, const uint32_t *__restrict__ 
       st += ss[w];
       vt += sv[w];
     }
-    if (SRC == SRC_PEERS && peers.n_acc > 0) {
+    if constexpr (SRC == SRC_NVLS || SRC == SRC_ONE) {
+      mc_red_add64<SRC == SRC_NVLS>(peers.acc_mc + 2 * slot, st);  // into every rank's slot
+      mc_red_add64<SRC == SRC_NVLS>(peers.acc_mc + 2 * slot + 1, vt);
+    } else if (SRC == SRC_PEERS && peers.n_acc > 0) {
       for (uint32_t r = 0; r < peers.n_acc; ++r) {
         atomicAdd(peers.acc[r] + 2 * slot, st);
         atomicAdd(peers.acc[r] + 2 * slot + 1, vt);
@@ -483,8 +565,28 @@ struct InitFn {
   }
 };
 
+template <int ZB, int SRC>
+cudaError_t launch_nvls_zb(const DevParams &p, bool fast, uint32_t addk, uint32_t slot, uint64_t q0,
+                           uint64_t q1, const vbdr_launch::Peers &pe, cudaStream_t s) {
+  const uint64_t work = q1 - q0;
+  if (fast)
+    return launch(k_slide<true, ZB, SRC>, grid_for(k_slide<true, ZB, SRC>, work), kThreads, 0, s,
+                  p, addk, slot, (const uint32_t *)nullptr, q0, q1, pe);
+  if (p.est == 2)
+    return launch(k_slide<false, ZB, SRC, true>, grid_for(k_slide<false, ZB, SRC, true>, work),
+                  kThreads, 0, s, p, addk, slot, (const uint32_t *)nullptr, q0, q1, pe);
+  return launch(k_slide<false, ZB, SRC>, grid_for(k_slide<false, ZB, SRC>, work), kThreads, 0, s,
+                p, addk, slot, (const uint32_t *)nullptr, q0, q1, pe);
+}
+
 template <int ZB>
 struct SlideFn {
+  template <int SRC>
+  static cudaError_t launch_nvls(const DevParams &p, bool fast, uint32_t addk, uint32_t slot,
+                                 uint64_t q0, uint64_t q1, const vbdr_launch::Peers &pe,
+                                 cudaStream_t s) {
+    return launch_nvls_zb<ZB, SRC>(p, fast, addk, slot, q0, q1, pe, s);
+  }
   static cudaError_t run(const DevParams &p, bool fast, const uint32_t *delta4, uint64_t q0,
                          uint64_t q1, const vbdr_launch::Peers *peers, cudaStream_t s) {
     // (2^zb - k) at every even field's LSB (Swar::active)
@@ -493,6 +595,8 @@ struct SlideFn {
     const uint32_t slot = p.tick & 3u;  // four slots: the estimate of tick T-1 may still read its own
     const uint64_t work = q1 - q0;
     const vbdr_launch::Peers none{};
+    if (peers && peers->nvls == 1) return launch_nvls<SRC_NVLS>(p, fast, addk, slot, q0, q1, *peers, s);
+    if (peers && peers->nvls == 2) return launch_nvls<SRC_ONE>(p, fast, addk, slot, q0, q1, *peers, s);
     if (fast && peers)
       return launch(k_slide<true, ZB, SRC_PEERS>, grid_for(k_slide<true, ZB, SRC_PEERS>, work),
                     kThreads, 0, s, p, addk, slot, (const uint32_t *)nullptr, q0, q1, *peers);
@@ -560,6 +664,11 @@ cudaError_t slide_peers(const DevParams &p, const Peers &peers, uint64_t j0, uin
                         cudaStream_t s) {
   return dispatch_zb<SlideFn>(p.zb, p, true, (const uint32_t *)nullptr, j0 >> 2, j1 >> 2, &peers,
                               s);
+}
+
+cudaError_t slide_multicast(const DevParams &p, const Peers &mc, uint64_t j0, uint64_t j1,
+                            bool fast, cudaStream_t s) {
+  return dispatch_zb<SlideFn>(p.zb, p, fast, (const uint32_t *)nullptr, j0 >> 2, j1 >> 2, &mc, s);
 }
 
 cudaError_t delta(const DevParams &p, uint8_t *out, cudaStream_t s) {

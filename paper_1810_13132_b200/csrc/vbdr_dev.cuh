@@ -153,6 +153,14 @@ struct Peers {
   uint8_t *regmax[kMaxPeers];            // every rank's regmax, or n_regmax = 0
   unsigned long long *acc[kMaxPeers];    // every rank's accumulator base, or n_acc = 0
   uint32_t n, n_regmax, n_acc;
+  // NVLS (vbdr_slide_multicast): multicast addresses of the state regions;
+  // nvls = 1 selects the multicast slide (then the arrays above are unused);
+  // 2 = the same for a group of one, through ordinary addresses
+  uint32_t nvls;
+  const uint32_t *sr_mc;                 // stamps (layout fast)
+  uint32_t *drv_mc;                      // packed DRV planes (layout packed)
+  uint8_t *regmax_mc;                    // the register buffer the slide writes
+  unsigned long long *acc_mc;            // accumulator base
 };
 cudaError_t init(const DevParams &p, bool fast, cudaStream_t s);
 cudaError_t scan(const DevParams &p, bool fast, int mode, const uint32_t *pairs, uint64_t n,
@@ -163,6 +171,8 @@ cudaError_t slide_delta(const DevParams &p, const uint8_t *delta, uint64_t j0, u
 cudaError_t delta(const DevParams &p, uint8_t *out, cudaStream_t s);
 cudaError_t slide_peers(const DevParams &p, const Peers &peers, uint64_t j0, uint64_t j1,
                         cudaStream_t s);
+cudaError_t slide_multicast(const DevParams &p, const Peers &mc, uint64_t j0, uint64_t j1,
+                            bool fast, cudaStream_t s);
 cudaError_t gather_words(const DevParams &p, const uint64_t *idx, uint64_t n, uint32_t *out,
                          cudaStream_t s);
 

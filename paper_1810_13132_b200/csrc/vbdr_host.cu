@@ -616,6 +616,33 @@ vbdr_status vbdr_slide_peers(vbdr_t *h, const uint8_t *const *h_peer_delta, uint
   return after_slide(h, stream);
 }
 
+vbdr_status vbdr_slide_multicast(vbdr_t *h, void *d_mc_state, uint64_t j0, uint64_t j1,
+                                 void *stream) {
+  if (!h) return VBDR_EINVAL;
+  if (!d_mc_state || (reinterpret_cast<uintptr_t>(d_mc_state) & 255u) || j0 >= j1 ||
+      j1 > h->p.n_phys || (j0 & 3u) || (j1 & 3u))
+    return fail(h, VBDR_EINVAL,
+                "need a 256-byte aligned multicast state address and 0 <= j0 < j1 <= n_phys, "
+                "both multiples of 4");
+  if (h->fast ? !drv_covers(h, j0, j1) : h->cfg.drv_shards > 1)
+    return fail(h, VBDR_EINVAL, h->fast ? "[j0, j1) outside this handle's DRV shard"
+                                        : "layout packed keeps a full DRV replica per rank");
+  // the multicast object maps every rank's state buffer, laid out like this one
+  uint8_t *mc = static_cast<uint8_t *>(d_mc_state);
+  const uint8_t *base = reinterpret_cast<const uint8_t *>(h->p.acc) - h->info.off_acc;
+  vbdr_launch::Peers pe{};
+  // a group of one without a multicast object: the handle's own state
+  pe.nvls = mc == base ? 2u : 1u;
+  pe.sr_mc = h->fast ? reinterpret_cast<const uint32_t *>(mc + h->info.off_sr) : nullptr;
+  pe.drv_mc = h->fast ? nullptr : reinterpret_cast<uint32_t *>(mc + h->info.off_drv);
+  pe.regmax_mc = mc + (h->p.regmax - base);  // the buffer this slide writes
+  pe.acc_mc = reinterpret_cast<unsigned long long *>(mc + h->info.off_acc);
+  if (vbdr_status s = check_async(h, "before slide_multicast")) return s;
+  const cudaError_t e = vbdr_launch::slide_multicast(h->p, pe, j0, j1, h->fast, S(stream));
+  if (e != cudaSuccess) return cuda_fail(h, e, "slide_multicast launch");
+  return after_slide(h, stream);
+}
+
 vbdr_status vbdr_select_above(vbdr_t *h, const double *d_est, uint64_t n, double threshold,
                               uint32_t *d_idx, uint64_t *d_count, void *stream) {
   if (!h || (n && (!d_est || !d_idx)) || !d_count) return VBDR_EINVAL;

@@ -49,7 +49,8 @@ SYMBOLS = ("vbdr_state_bytes", "vbdr_create", "vbdr_destroy", "vbdr_scan_slice",
            "vbdr_host_sums_plan", "vbdr_plan_check", "vbdr_plan_release",
            "vbdr_estimate_plan_host", "vbdr_config_check", "vbdr_select_above",
            "vbdr_sparse_extract", "vbdr_sparse_apply", "vbdr_last_error", "vbdr_status_string",
-           "vbdr_plan_bytes_kind", "vbdr_plan_build_kind")
+           "vbdr_plan_bytes_kind", "vbdr_plan_build_kind", "vbdr_slide_multicast",
+           "vbdr_mc_alloc", "vbdr_mc_free", "vbdr_mc_last_error")
 PLAN_KINDS = {"auto": 0, "staged": 1, "passid": 2, "sorted": 3}
 
 _lib = None
@@ -81,6 +82,9 @@ def lib():
             "vbdr_sparse_apply": [vp, vp, u64, vp, vp],
             "vbdr_debug_set_tick": [vp, u32],
             "vbdr_slide_peers": [vp, vp, u32, u64, u64, vp, vp, vp],
+            "vbdr_slide_multicast": [vp, vp, u64, u64, vp],
+            "vbdr_mc_alloc": [u64, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64)],
+            "vbdr_mc_free": [vp],
             "vbdr_plan_bytes": [vp, u64, C.POINTER(u64)],
             "vbdr_plan_build": [vp, vp, u64, vp, u64, vp],
             "vbdr_plan_bytes_kind": [vp, u64, u32, C.POINTER(u64)],
@@ -104,6 +108,8 @@ def lib():
         L.vbdr_last_error.restype = C.c_char_p
         L.vbdr_config_check.argtypes = [C.POINTER(vbdr_config)]
         L.vbdr_config_check.restype = C.c_char_p
+        L.vbdr_mc_last_error.argtypes = []
+        L.vbdr_mc_last_error.restype = C.c_char_p
         L.vbdr_status_string.argtypes = [C.c_int]
         L.vbdr_status_string.restype = C.c_char_p
         _lib = L
@@ -260,11 +266,28 @@ class VBDR:
             raise RuntimeError("vbdr_sparse_extract: cap too small")
         return records, counts
 
+    def sparse_extract_into(self, records, counts, stream=None):
+        """``vbdr_sparse_extract`` into caller buffers, no host read: records
+        int32[n_owners, cap] (slots past an owner's count are left as they
+        were), counts int64[n_owners] (the exact totals, possibly > cap)."""
+        n_owners, cap = records.shape
+        assert records.is_contiguous() and counts.numel() == n_owners
+        self._check(lib().vbdr_sparse_extract(self._h, n_owners, C.c_void_p(records.data_ptr()),
+                                              cap, C.c_void_p(counts.data_ptr()),
+                                              _stream_ptr(stream)), "vbdr_sparse_extract")
+
     def sparse_apply(self, records, delta_shard, stream=None):
         """``vbdr_sparse_apply``: per-byte max of received records into a shard."""
         self._check(lib().vbdr_sparse_apply(self._h, C.c_void_p(records.data_ptr()),
                                             records.numel(), C.c_void_p(delta_shard.data_ptr()),
                                             _stream_ptr(stream)), "vbdr_sparse_apply")
+
+    def slide_multicast(self, mc_state: int, j0: int = 0, j1: int | None = None, stream=None):
+        """``vbdr_slide_multicast``: fused NVLS merge + slide of BDRs [j0, j1);
+        mc_state is the multicast address of every rank's state buffer."""
+        j1 = self.n_phys if j1 is None else j1
+        self._check(lib().vbdr_slide_multicast(self._h, C.c_void_p(mc_state), j0, j1,
+                                               _stream_ptr(stream)), "vbdr_slide_multicast")
 
     def slide_delta(self, delta, j0: int = 0, j1: int | None = None, stream=None):
         """``vbdr_slide_delta``: close the slice from a merged delta over [j0, j1)."""
@@ -467,6 +490,79 @@ class EstimatePlan:
         self.buf = None
 
 
+class McBuffer:
+    """``vbdr_mc_alloc``: device memory bound to a one-device multicast object
+    (one GPU: the multicast slide's test path).  ``tensor`` is a uint8 view of
+    the unicast mapping (pass it as ``VBDR(state=...)``), ``mc`` the multicast
+    address of the same bytes.  Raises RuntimeError without multicast support."""
+
+    class _Iface:
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1",
+                                             "data": (ptr, False), "version": 3}
+
+    def __init__(self, nbytes: int, device=None):
+        import torch
+        uc, mc, got = C.c_void_p(), C.c_void_p(), C.c_uint64()
+        with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
+            rc = lib().vbdr_mc_alloc(nbytes, C.byref(uc), C.byref(mc), C.byref(got))
+        if rc != 0:
+            raise RuntimeError(f"vbdr_mc_alloc failed: {STATUS.get(rc, rc)}: "
+                               f"{lib().vbdr_mc_last_error().decode()}")
+        self.uc, self.mc, self.nbytes = uc.value, mc.value, got.value
+        self.tensor = torch.as_tensor(McBuffer._Iface(self.uc, self.nbytes),
+                                      device=torch.device("cuda", torch.cuda.current_device()))
+
+    def free(self):
+        if self.uc:
+            self.tensor = None
+            lib().vbdr_mc_free(C.c_void_p(self.uc))
+            self.uc = None
+
+
+class NvlsMerge:
+    """Fused NVLS merge + slide (``vbdr_slide_multicast``) for
+    both layouts.  Every rank's pool state lives in torch symmetric memory
+    bound to one multicast object; each rank closes its BDR shard with one
+    kernel whose loads are reduced by the NVSwitch (MAX of stamps, or AND of
+    packed DRV words) and whose registers, pool sums (and packed DRV words)
+    land in every rank.  Two device-side barriers (symmetric-memory signal
+    pads, no NCCL call) order it after every rank's scan and before the next
+    scan or estimate.  The pool must be created with
+    ``state=NvlsMerge.alloc_state(...)``.  With one GPU, ``McBuffer`` gives the
+    same kernel a one-device multicast object (tests/test_gpu_parity.py)."""
+
+    @staticmethod
+    def alloc_state(cfg, device):
+        import torch
+        import torch.distributed._symmetric_memory as symm
+        return symm.empty(state_bytes(cfg), dtype=torch.uint8, device=device)
+
+    def __init__(self, pool: "VBDR", group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.pool, self.group = pool, group
+        self.world, self.rank = _world(group)
+        grp = group if group is not None else dist.group.WORLD
+        self.handle = symm.rendezvous(pool.state, grp)
+        self.mc = int(self.handle.multicast_ptr)
+        if not self.mc:
+            raise RuntimeError("no multicast object for this group (NVLS unavailable)")
+        n = pool.n_phys // self.world
+        if n * self.world != pool.n_phys or n % 4:
+            raise ValueError("nvls merge needs n_phys divisible by 4 * world size")
+        self.j0, self.j1 = self.rank * n, (self.rank + 1) * n
+
+    def close_slice(self, on_merged=None, on_slid=None):
+        self.handle.barrier(channel=0)  # every rank's scan of the slice is done
+        if on_merged is not None:
+            on_merged()
+        self.pool.slide_multicast(self.mc, self.j0, self.j1)
+        if on_slid is not None:
+            on_slid()
+        self.handle.barrier(channel=1)  # every rank's registers and sums have landed
+
+
 # ------------------------------------------------------------ multi-GPU plumbing
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous [start, stop) of n units for rank (pairs of a slice, or hosts).
@@ -497,7 +593,7 @@ def merge_stamps(pool: "VBDR", group=None):
     return merge_stamps_tensor(pool.sr_view(), group)
 
 
-MERGE_MODES = ("stamps", "delta", "sharded", "sparse", "p2p")
+MERGE_MODES = ("stamps", "delta", "sharded", "sparse", "p2p", "nvls")
 
 
 def _world(group):
@@ -563,19 +659,20 @@ class PeerMerge:
         self.delta = symm.empty(pool.n_phys, dtype=torch.uint8, device=pool.device)
         hd = symm.rendezvous(self.delta, grp)
         hs = symm.rendezvous(pool.state, grp)
+        self.handle = hd
         inf = pool.info()
         self.peer_delta = [hd.buffer_ptrs[r] for r in range(self.world)]
         self.peer_base = [hs.buffer_ptrs[r] for r in range(self.world)]
         self.peer_acc = [hs.buffer_ptrs[r] + inf["off_acc"] for r in range(self.world)]
-        self.flag = torch.zeros(1, dtype=torch.int32, device=pool.device)
         n = pool.n_phys // self.world
         if n * self.world != pool.n_phys or n % 4:
             raise ValueError("p2p merge needs n_phys divisible by 4 * world size")
         self.j0, self.j1 = self.rank * n, (self.rank + 1) * n
 
-    def _barrier(self):
-        import torch.distributed as dist
-        dist.all_reduce(self.flag, group=self.group)  # stream-ordered across ranks
+    def _barrier(self, channel: int = 0):
+        # device-side barrier over the symmetric-memory signal pads: a tiny
+        # kernel on the current stream, no NCCL call, no host synchronisation
+        self.handle.barrier(channel=channel)
 
     def peer_regmax_next(self) -> list:
         """Every rank's register buffer that the next slide writes (it
@@ -589,14 +686,14 @@ class PeerMerge:
         callbacks run after the first barrier and after the slide launch
         (bench.py records its phase events there)."""
         self.pool.stamp_delta(self.delta)
-        self._barrier()  # every rank's delta is written
+        self._barrier(0)  # every rank's delta is written
         if on_merged is not None:
             on_merged()
         self.pool.slide_peers(self.peer_delta, self.j0, self.j1, self.peer_regmax_next(),
                               self.peer_acc)
         if on_slid is not None:
             on_slid()
-        self._barrier()  # every rank's register shard and sums have landed
+        self._barrier(1)  # every rank's register shard and sums have landed
 
 
 def slide_merged(pool: "VBDR", group=None, mode: str = "sharded", delta=None, shard=None):
@@ -644,29 +741,91 @@ def slide_merged(pool: "VBDR", group=None, mode: str = "sharded", delta=None, sh
     dist.all_reduce(pool.acc_view(), op=dist.ReduceOp.SUM, group=group)
 
 
+class SparseMerge:
+    """slide_merged(mode="sparse") without host synchronisation on the slice
+    path (SURVEY 8(e) iii).  Each rank lists the BDRs its pairs touched as u32
+    records per owner shard (``vbdr_sparse_extract``) into a FIXED-capacity
+    buffer ``[world, cap]``; one equal-split all-to-all moves every rank's
+    ``cap`` records per owner; unused slots stay zero, and a zero record
+    (BDR 0, rank 0) is a no-op of ``vbdr_sparse_apply``'s per-byte max.  The
+    owner folds the records into its u8 delta shard, slides it, and the
+    registers are all-gathered, the pool sums all-reduced.
+
+    ``cap`` is sized once from the exact counts of the first slice (the only
+    host read, before any timed work) with ``headroom``, agreed by MAX over
+    the ranks.  Later slices never read counts on the host: a device-side
+    running maximum is kept, and :meth:`check` (call it after the timed
+    region) raises if any owner ever needed more than ``cap`` records --
+    records beyond it would have been dropped."""
+
+    def __init__(self, pool: "VBDR", group=None, cap: int | None = None, headroom: float = 1.25):
+        import torch
+        self.pool, self.group = pool, group
+        self.world, self.rank = _world(group)
+        n = pool.n_phys // self.world
+        if n * self.world != pool.n_phys or n % 4:
+            raise ValueError("sparse merge needs n_phys divisible by 4 * world size")
+        self.n, self.cap, self.headroom = n, cap, headroom
+        dev = pool.device
+        self.shard = torch.empty(n, dtype=torch.uint8, device=dev)
+        self.counts = torch.empty(self.world, dtype=torch.int64, device=dev)
+        self.max_count = torch.zeros((), dtype=torch.int64, device=dev)
+        self.records = self.recv = None
+        if cap is not None:
+            self._alloc(cap)
+
+    def _alloc(self, cap: int):
+        import torch
+        self.cap = int(cap)
+        dev = self.pool.device
+        self.records = torch.zeros((self.world, self.cap), dtype=torch.int32, device=dev)
+        self.recv = torch.empty(self.world * self.cap, dtype=torch.int32, device=dev)
+
+    def _size_from_first_slice(self):
+        import torch
+        import torch.distributed as dist
+        lib_ = lib()
+        self.pool._check(lib_.vbdr_sparse_extract(self.pool._h, self.world, None, 0,
+                                                  C.c_void_p(self.counts.data_ptr()),
+                                                  _stream_ptr(None)), "vbdr_sparse_extract")
+        want = torch.tensor([int(self.counts.max())], dtype=torch.int64, device=self.pool.device)
+        if self.world > 1:
+            dist.all_reduce(want, op=dist.ReduceOp.MAX, group=self.group)
+        cap = max(1024, int(int(want) * self.headroom + 1023) // 1024 * 1024)
+        self._alloc(cap)
+
+    def close_slice(self):
+        import torch
+        import torch.distributed as dist
+        if self.cap is None:
+            self._size_from_first_slice()
+        self.records.zero_()  # zero record = (BDR 0, rank 0): a no-op of sparse_apply
+        self.pool.sparse_extract_into(self.records, self.counts)
+        torch.maximum(self.max_count, self.counts.max(), out=self.max_count)
+        _all_to_all(self.recv, self.records.view(-1), None, None, self.group)
+        self.shard.zero_()
+        self.pool.sparse_apply(self.recv, self.shard)
+        self.pool.slide_delta(self.shard, self.rank * self.n, (self.rank + 1) * self.n)
+        all_gather_shards(self.pool.regmax_view(), self.group)
+        dist.all_reduce(self.pool.acc_view(), op=dist.ReduceOp.SUM, group=self.group)
+
+    def check(self):
+        """Host check after the timed region: raises if records were dropped."""
+        need = int(self.max_count)
+        if self.cap is not None and need > self.cap:
+            raise RuntimeError(f"sparse merge overflow: an owner needed {need} records, cap "
+                               f"{self.cap} (records were dropped: raise cap or headroom)")
+        return need
+
+
 def _slide_sparse(pool: "VBDR", group, world: int, rank: int, shard=None):
-    """slide_merged(mode="sparse"): records of touched BDRs, all-to-all by
-    owner shard, per-byte max into the own delta shard, sharded slide."""
-    import torch
-    import torch.distributed as dist
-    n = pool.n_phys // world
-    if n * world != pool.n_phys or n % 4:
-        raise ValueError("sparse merge needs n_phys divisible by 4 * world size")
-    records, counts = pool.sparse_extract(world)
-    recv_counts = torch.empty_like(counts)
-    _all_to_all(recv_counts, counts, None, None, group)
-    send_sizes = counts.tolist()
-    recv_sizes = recv_counts.tolist()
-    send = torch.cat([records[o, :send_sizes[o]] for o in range(world)])
-    recv = torch.empty(sum(recv_sizes), dtype=torch.int32, device=records.device)
-    _all_to_all(recv, send, recv_sizes, send_sizes, group)
-    if shard is None:
-        shard = torch.empty(n, dtype=torch.uint8, device=records.device)
-    shard.zero_()
-    pool.sparse_apply(recv, shard)
-    pool.slide_delta(shard, rank * n, (rank + 1) * n)
-    all_gather_shards(pool.regmax_view(), group)
-    dist.all_reduce(pool.acc_view(), op=dist.ReduceOp.SUM, group=group)
+    """slide_merged(mode="sparse") through the pool's SparseMerge (created on
+    first use for this group)."""
+    sm = getattr(pool, "_sparse_merge", None)
+    if sm is None or sm.group is not group:
+        sm = SparseMerge(pool, group)
+        pool._sparse_merge = sm
+    sm.close_slice()
 
 
 def _all_to_all(out, inp, out_sizes, in_sizes, group=None):

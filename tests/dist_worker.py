@@ -52,6 +52,8 @@ def main(mode: str):
                 int((M == 0).sum()))
             if mode == "stamps" or mode == "delta":  # every replica slides all BDRs
                 ok &= np.array_equal(pool.export_ages(), ref.drv())
+    if mode == "sparse":  # the fixed-capacity record buffers never overflowed
+        ok &= pool._sparse_merge.check() <= pool._sparse_merge.cap
     hosts = tr.host_ids()
     h0, h1 = shard_range(len(hosts), rank, world)
     est = pool.estimate(torch.from_numpy(hosts[h0:h1].view(np.int32)).to(dev)).cpu()

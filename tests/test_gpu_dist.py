@@ -38,10 +38,24 @@ def test_slide_merged_multi_rank(mode, world):
     assert f"parity=ok" in r.stdout
 
 
-def test_bench_two_ranks_gloo_same_device():
+@pytest.mark.parametrize("merge", ["sharded", "sparse"])
+def test_bench_two_ranks_gloo_same_device(merge):
     r = _torchrun(2, "bench.py", "--gpus", "2", "--steps", "5", "--warmup", "3", "--config", "tiny",
-                  "--dist-backend", "gloo", "--same-device", "--no-cpu-baseline")
+                  "--dist-backend", "gloo", "--same-device", "--no-cpu-baseline", "--merge", merge)
     assert r.returncode == 0, r.stderr[-4000:]
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
-    assert "merge=sharded" in line["config"]["parallelism"]
+    assert f"merge={merge}" in line["config"]["parallelism"]
+    assert "communicator of 2 ranks" in r.stderr
+
+
+@pytest.mark.parametrize("layout", ["fast", "packed"])
+def test_bench_one_gpu_multicast_slide(layout):
+    """bench.py --merge nvls on one GPU: the NVLS merge + slide kernel through a
+    one-device multicast object inside the timed steps."""
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "4", "--warmup", "3", "--config",
+                        "tiny", "--merge", "nvls", "--layout", layout, "--no-cpu-baseline"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-4000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert "multicast" in line["config"]["parallelism"] and line["value"] > 0

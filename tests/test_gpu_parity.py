@@ -496,6 +496,15 @@ def test_loopback_delta_merge(mode, n_ranks):
         else:
             if mode == "sparse":
                 out = [pool.sparse_extract(n_ranks) for pool in ranks]
+                # SparseMerge's fixed-capacity form: zero-initialised rows of
+                # a larger cap (slots past each count stay zero)
+                cap = max(int(c.max()) for _, c in out) + 37
+                rows_all = []
+                for src in ranks:
+                    rows = torch.zeros((n_ranks, cap), dtype=torch.int32, device=DEV)
+                    cnt = torch.empty(n_ranks, dtype=torch.int64, device=DEV)
+                    src.sparse_extract_into(rows, cnt)
+                    rows_all.append(rows)
                 for src, (rec, cnt) in enumerate(out):  # the touched BDRs, exactly
                     d = deltas[src].cpu().numpy()
                     for o in range(n_ranks):
@@ -509,6 +518,11 @@ def test_loopback_delta_merge(mode, n_ranks):
                     for rec, cnt in out:
                         pool.sparse_apply(rec[r, :int(cnt[r])].contiguous(), shard)
                     assert torch.equal(shard, merged[r * n:(r + 1) * n])
+                    # the padded rows applied whole: zero records are no-ops
+                    padded = torch.zeros(n, dtype=torch.uint8, device=DEV)
+                    for rows in rows_all:
+                        pool.sparse_apply(rows[r].contiguous(), padded)
+                    assert torch.equal(padded, shard)
                 else:
                     shard = merged[r * n:(r + 1) * n].clone()
                 pool.slide_delta(shard, r * n, (r + 1) * n)
@@ -894,3 +908,93 @@ def test_query_top_super_spreaders():
     a2, e2 = pool.query_top(hosts, 100.0, plan=plan)
     a1, e1 = pool.query_top(hosts, 100.0)
     assert np.array_equal(a1, a2) and np.array_equal(e1, e2)
+
+
+@pytest.mark.parametrize("via", ["self", "multicast"])
+@pytest.mark.parametrize("layout,estimator", [("fast", "hll"), ("packed", "hll"),
+                                              ("packed", "pcsa"), ("fast", "loglog")])
+def test_nvls_slide_one_device(layout, estimator, via):
+    """vbdr_slide_multicast (the fused NVLS merge + slide) for a
+    group of one GPU: "multicast" through a one-device multicast object
+    (vbdr_mc_alloc: multimem.ld_reduce MAX of the stamps / AND of the packed
+    words, multimem.st of registers and words, multimem.red of the pool
+    sums); "self" with the handle's own state as the group address (the same
+    kernel, the multimem operations replaced by what they reduce to over one
+    member).  Every boundary of 11 slices (past k: expired, unsaturated DRs)
+    is bit-exact against the oracle; estimates within 1e-9."""
+    from paper_1810_13132_b200 import McBuffer, make_config, state_bytes
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    buf = None
+    state = None
+    if via == "multicast":
+        nbytes = state_bytes(make_config(32, 4, 1 << 12, layout=layout, estimator=estimator))
+        try:
+            buf = McBuffer(nbytes, DEV)
+        except RuntimeError as e:  # e.g. cuMulticastCreate refused in this container
+            pytest.skip(f"no multicast object on this device: {e}")
+        state = buf.tensor
+    try:
+        pool = VBDR(32, 4, 1 << 12, layout=layout, estimator=estimator, device=DEV, state=state)
+        mc = buf.mc if buf is not None else pool.state.data_ptr()
+        ref = oracle.Pool(cfg, "serial" if layout == "fast" else "gsmall")
+        hosts_np = tr.host_ids()
+        hosts = dev_u32(hosts_np)
+        slices = []
+        for t in range(11):
+            pairs = synth.generate(tr, t)
+            slices.append(pairs)
+            pool.scan_slice(dev_u32(pairs))
+            pool.slide_multicast(mc)
+            ref.slice(pairs)
+            if estimator == "hll":
+                compare_boundary(pool, ref, [], hosts_np, hosts, np.concatenate(slices[-4:]))
+                continue
+            V = ref.readout_pcsa() if estimator == "pcsa" else ref.readout()
+            assert np.array_equal(pool.export_regmax(), V)
+            assert pool.export_pool_sums() == (int(V.astype(np.int64).sum()), int((V == 0).sum()))
+            est = pool.estimate(hosts).cpu().numpy()
+            want = oracle.estimate_variant(V, hosts_np, cfg.b, cfg.z, estimator)
+            check_estimates(est, want, variant_floor(V, hosts_np, cfg.b, cfg.z, estimator))
+        assert pool.info()["slices_closed"] == 11
+        pool.close()
+        torch.cuda.synchronize()
+    finally:
+        if buf is not None:
+            buf.free()
+
+
+def test_nvls_slide_shard_self():
+    """The multicast slide over a register-sharded handle's shard [j0, j1)
+    (layout fast, drv_shards = 2): a rank of two closes its shard; ranges
+    outside the shard are refused."""
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial")
+    n = cfg.z // 2
+    pools = [VBDR(32, 4, 1 << 12, device=DEV, drv_shards=2, drv_shard=r) for r in range(2)]
+    with pytest.raises(RuntimeError):
+        pools[0].slide_multicast(pools[0].state.data_ptr(), n, 2 * n)  # not its shard
+    for t in range(7):
+        pairs = synth.generate(tr, t)
+        ref.slice(pairs)
+        for r, pool in enumerate(pools):
+            pool.scan_slice(dev_u32(pairs))  # the whole slice on both (no merge to emulate)
+            pool.slide_multicast(pool.state.data_ptr(), r * n, (r + 1) * n)
+        M = ref.readout()
+        for r, pool in enumerate(pools):
+            assert np.array_equal(pool.export_regmax()[r * n:(r + 1) * n], M[r * n:(r + 1) * n])
+            ages = pool.export_ages_at(np.arange(r * n, (r + 1) * n, dtype=np.uint64))
+            assert np.array_equal(ages, ref.drv()[r * n:(r + 1) * n])
+
+
+def test_nvls_slide_rejects_bad_ranges():
+    pool = VBDR(32, 4, 1 << 12, device=DEV)
+    base = pool.state.data_ptr()
+    for j0, j1 in ((0, 0), (2, 64), (0, (1 << 12) + 4)):
+        with pytest.raises(RuntimeError):
+            pool.slide_multicast(base, j0, j1)
+    with pytest.raises(RuntimeError):
+        pool.slide_multicast(base + 16)  # not 256-byte aligned
+    packed = VBDR(32, 4, 1 << 12, layout="packed", device=DEV)
+    packed.slide_multicast(packed.state.data_ptr())  # full range: fine
