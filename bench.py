@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="vbdr", choices=["vbdr", "reference"])
     ap.add_argument("--config", default="caida", choices=list(WORKLOADS))
-    ap.add_argument("--layout", default="fast", choices=["fast", "packed"])
+    ap.add_argument("--layout", default="fast", choices=["fast", "packed", "stamps"])
     ap.add_argument("--scan-mode", type=int, default=0)
     ap.add_argument("--est-lanes", type=int, default=0)
     ap.add_argument("--est-pass-log2", type=int, default=0)
@@ -145,7 +145,10 @@ def table1_bits(m: int, k: int) -> dict:
 
 def algorithmic_bytes_per_bdr(layout: str, words: int) -> int:
     """Slide kernel, per physical BDR: read sr (4 B, fast only), read+write W
-    packed DRV words (8 W B), write the register value (1 B).  DESIGN.md s.6."""
+    packed DRV words (8 W B), write the register value (1 B); layout stamps:
+    read the L stamps (4 L B, words = L), write the register.  DESIGN.md s.6."""
+    if layout == "stamps":
+        return 4 * words + 1
     return (4 if layout == "fast" else 0) + 8 * words + 1
 
 
@@ -348,9 +351,11 @@ def run_vbdr(args):
 
     tr = synth.CONFIGS[args.config]
     wl = WORKLOADS[args.config]
-    if world > 1 and args.layout != "fast" and args.merge != "nvls":
+    if world > 1 and args.layout == "packed" and args.merge != "nvls":
         raise SystemExit("multi-GPU layout packed needs --merge nvls (NCCL has no bitwise-AND "
                          "reduction; the NVSwitch multimem.ld_reduce has)")
+    if world > 1 and args.layout == "stamps" and args.merge != "stamps":
+        raise SystemExit("multi-GPU layout stamps merges with --merge stamps (allreduce MAX)")
     if world > 1:
         print(f"rank {rank}: {args.dist_backend} communicator of {dist.get_world_size()} ranks, "
               f"device {torch.cuda.get_device_name(dev)} (cuda:{gpu})", file=sys.stderr, flush=True)
@@ -771,6 +776,7 @@ def run_vbdr(args):
                    "plan_bytes": plan.nbytes if plan is not None else None,
                    "zbits": info["zbits"], "words_per_bdr": info["words"],
                    "bits_per_bdr": (32 if args.layout == "fast" else 0) + 32 * info["words"],
+                   "state_bytes": info["state_bytes"],
                    "table1_bits_per_bdr": table1_bits(wl["m"], wl["k"])},
         "scan_mpairs_s": round(tr.pairs_per_slice / (kern["scan"] * 1e-3) / 1e6, 2),
         "slide_ms": round(kern["slide"], 5), "estimate_ms": round(kern["estimate"], 5),

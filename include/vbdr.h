@@ -52,7 +52,17 @@ typedef enum {
     /* Packed DRV only, every rank recorded with atomicAnd (Alg.9)
      * and aged at the slide (Alg.8 hoisted).  VBDR-gsmall
      * semantics, the memory-efficient variant (Table 1). */
-    VBDR_LAYOUT_PACKED = 1
+    VBDR_LAYOUT_PACKED = 1,
+    /* Layout S: a u32 last-seen stamp per (BDR, rank) -- the literal "stamps"
+     * reading of the north star, with VBDR-gsmall semantics: the scan records
+     * every pair's rank (as Alg.9's SetDR) with
+     * atomicMax(stamp[rho-1][pidx], T); nothing is aged, a DR's age is
+     * T - stamp at readout (IsActiveDR).  32 L bits per BDR: a
+     * comparison point for the two packed layouts.  Single
+     * GPU or the "stamps" merge (allreduce MAX of all stamps); scan_mode 2 or
+     * 5 (5 only while L * n_phys < 2^32).  Ages export as T - stamp (0xFFFF
+     * never recorded; canonical: min(age, k)). */
+    VBDR_LAYOUT_STAMPS = 2
 } vbdr_layout;
 
 typedef struct {

@@ -154,6 +154,142 @@ k_scan(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict
   pdl_trigger();  // this block's work is issued: let the next kernel launch
 }
 
+// ----------------------------------------------------- layout S (stamps)
+// Layout S (the north star's literal "last-seen-slice stamps"
+// reading, with VBDR-gsmall semantics): a u32 stamp per (BDR j, rank rho) =
+// the tick T of the last slice in which rho was recorded into j, in L planes
+// of n_phys words (plane rho - 1).  The scan records EVERY pair's rank (as
+// Alg.9's per-pair SetDR) as atomicMax(stamp, T); nothing
+// ever ages: a DR's age is T - stamp, computed at readout.  32 L bits per BDR
+// (caida: 800, against 75 for Table 1's gsmall) -- the comparison point for
+// the packed layouts, not a default.
+template <int MODE>
+__device__ __forceinline__ void record_stamp(uint32_t aip, uint32_t bip, const DevParams &p,
+                                             ScanCache *cache) {
+  uint32_t pidx, rho;
+  pair_index(aip, bip, p, pidx, rho);  // Alg.4
+  const uint64_t word = (uint64_t)(rho - 1u) * p.n_phys + pidx;
+  uint32_t *a = p.drv + word;
+  const uint32_t val = p.tick;
+  if constexpr (MODE == 5) {  // L * n_phys < 2^32 for this mode
+    const uint32_t key = (uint32_t)word + 1u;
+    if (cache_hit(cache, key, val, true)) return;
+    const uint32_t cur = ld_relaxed(a);
+    if (cur >= val) {
+      cache_put(cache, key, cur);
+      return;
+    }
+    atomicMax(a, val);
+    cache_put(cache, key, val);
+    return;
+  }
+  if (ld_relaxed(a) >= val) return;  // already stamped in this slice
+  atomicMax(a, val);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_stamps(const uint4 *__restrict__ pairs2, uint64_t n2, const uint32_t *__restrict__ tail,
+              DevParams p) {
+  pdl_wait();
+  constexpr int UNROLL = 4;
+  extern __shared__ unsigned long long scan_dyn_smem[];
+  ScanCache *cache = nullptr;
+  if constexpr (MODE == 5) {
+    cache = reinterpret_cast<ScanCache *>(scan_dyn_smem);
+    for (int s = threadIdx.x; s < kCacheSlots; s += kScanThreads) cache->e[s] = 0ull;
+    __syncthreads();
+  }
+  const uint64_t stride = (uint64_t)gridDim.x * kScanThreads;
+  uint64_t i = (uint64_t)blockIdx.x * kScanThreads + threadIdx.x;
+  for (; i + (UNROLL - 1) * stride < n2; i += UNROLL * stride) {
+    uint4 v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) v[u] = __ldcs(pairs2 + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      record_stamp<MODE>(v[u].x, v[u].y, p, cache);
+      if (v[u].z != v[u].x || v[u].w != v[u].y) record_stamp<MODE>(v[u].z, v[u].w, p, cache);
+    }
+  }
+  for (; i < n2; i += stride) {
+    const uint4 v = __ldcs(pairs2 + i);
+    record_stamp<MODE>(v.x, v.y, p, cache);
+    if (v.z != v.x || v.w != v.y) record_stamp<MODE>(v.z, v.w, p, cache);
+  }
+  if (tail != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+    record_stamp<MODE>(tail[0], tail[1], p, cache);
+  pdl_trigger();
+}
+
+// Close tick T for layout S: per BDR, the active ranks are those with a stamp
+// and T - stamp < k (IsActiveDR, on the derived age); M = the
+// highest (Alg.2), PCSA's R = the active run from rank 1.  Streams 4 L bytes
+// per BDR, writes nothing back but the register.
+template <bool PCSA>
+__global__ void __launch_bounds__(kThreads) k_slide_stamps(DevParams p, uint32_t slot) {
+  pdl_wait();
+  const uint64_t n4 = p.n_phys >> 2;
+  const uint4 *st4 = reinterpret_cast<const uint4 *>(p.drv);
+  uint32_t *reg4 = reinterpret_cast<uint32_t *>(p.regmax);
+  unsigned long long s_acc = 0;
+  uint32_t v_acc = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t q = (uint64_t)blockIdx.x * kThreads + threadIdx.x; q < n4; q += stride) {
+    uint32_t act[4] = {0u, 0u, 0u, 0u};  // bit rho - 1: rank rho active
+#pragma unroll 8
+    for (uint32_t r = 0; r < p.L; ++r) {
+      const uint4 s = __ldcs(st4 + (uint64_t)r * n4 + q);
+      const uint32_t sv[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        act[c] |= (uint32_t)(sv[c] != 0u && p.tick - sv[c] < p.k) << r;
+    }
+    uint32_t best[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if constexpr (PCSA)
+        best[c] = min((uint32_t)__ffs(~act[c]) - 1u, p.L);  // consecutive active from rank 1
+      else
+        best[c] = act[c] ? 32u - (uint32_t)__clz(act[c]) : 0u;
+    }
+    reg4[q] = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      s_acc += p.est == 0u ? 1ull << (p.L - best[c]) : (unsigned long long)best[c];
+      v_acc += best[c] == 0u;
+    }
+  }
+  pdl_trigger();
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    s_acc += __shfl_xor_sync(0xffffffffu, s_acc, off);
+    v_acc += __shfl_xor_sync(0xffffffffu, v_acc, off);
+  }
+  __shared__ unsigned long long ss[kThreads / 32];
+  __shared__ uint32_t sv[kThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    ss[warp] = s_acc;
+    sv[warp] = v_acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long st = 0, vt = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      st += ss[w];
+      vt += sv[w];
+    }
+    atomicAdd(p.acc + 2 * slot, st);
+    atomicAdd(p.acc + 2 * slot + 1, vt);
+    if (blockIdx.x == 0) {
+      p.acc[2 * ((slot + 1u) & 3u)] = 0ull;
+      p.acc[2 * ((slot + 1u) & 3u) + 1] = 0ull;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ slide
 // One thread = 4 consecutive BDRs (16-byte loads of every plane).
 //   FAST:   age all DRs (Alg.1), SetDR(DRV[nowLBP1]) if sr is from
@@ -669,6 +805,28 @@ cudaError_t slide_peers(const DevParams &p, const Peers &peers, uint64_t j0, uin
 cudaError_t slide_multicast(const DevParams &p, const Peers &mc, uint64_t j0, uint64_t j1,
                             bool fast, cudaStream_t s) {
   return dispatch_zb<SlideFn>(p.zb, p, fast, (const uint32_t *)nullptr, j0 >> 2, j1 >> 2, &mc, s);
+}
+
+cudaError_t scan_stamps(const DevParams &p, int mode, const uint32_t *pairs, uint64_t n,
+                        cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const uint64_t n2 = n >> 1;
+  const uint32_t *tail = (n & 1u) ? pairs + 2 * (n - 1) : nullptr;
+  const uint4 *pairs2 = reinterpret_cast<const uint4 *>(pairs);
+  const uint64_t work = n2 ? n2 : 1;
+  constexpr int T = kScanThreads;
+  if (mode == 5)
+    return launch(k_scan_stamps<5>, grid_for(k_scan_stamps<5>, work, T, sizeof(ScanCache)), T,
+                  sizeof(ScanCache), s, pairs2, n2, tail, p);
+  return launch(k_scan_stamps<2>, grid_for(k_scan_stamps<2>, work, T), T, 0, s, pairs2, n2, tail, p);
+}
+
+cudaError_t slide_stamps(const DevParams &p, cudaStream_t s) {
+  const uint32_t slot = p.tick & 3u;
+  const uint64_t work = p.n_phys >> 2;
+  if (p.est == 2)
+    return launch(k_slide_stamps<true>, grid_for(k_slide_stamps<true>, work), kThreads, 0, s, p, slot);
+  return launch(k_slide_stamps<false>, grid_for(k_slide_stamps<false>, work), kThreads, 0, s, p, slot);
 }
 
 cudaError_t delta(const DevParams &p, uint8_t *out, cudaStream_t s) {

@@ -166,6 +166,10 @@ cudaError_t init(const DevParams &p, bool fast, cudaStream_t s);
 cudaError_t scan(const DevParams &p, bool fast, int mode, const uint32_t *pairs, uint64_t n,
                  cudaStream_t s);
 cudaError_t slide(const DevParams &p, bool fast, cudaStream_t s);
+// layout S (per-(BDR, rank) stamps in the drv region, L planes)
+cudaError_t scan_stamps(const DevParams &p, int mode, const uint32_t *pairs, uint64_t n,
+                        cudaStream_t s);
+cudaError_t slide_stamps(const DevParams &p, cudaStream_t s);
 cudaError_t slide_delta(const DevParams &p, const uint8_t *delta, uint64_t j0, uint64_t j1,
                         cudaStream_t s);
 cudaError_t delta(const DevParams &p, uint8_t *out, cudaStream_t s);

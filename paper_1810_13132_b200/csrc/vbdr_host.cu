@@ -20,7 +20,8 @@ struct vbdr {
   vbdr_config cfg{};
   vbdr_info_t info{};
   DevParams p{};
-  bool fast = true;
+  bool fast = true;     // layout F
+  bool stamps = false;  // layout S (per-(BDR, rank) stamps)
   double alpha_g = 0, alpha_z = 0;
   std::string err;
   // host-buffer pipeline resources (created on first use)
@@ -93,7 +94,7 @@ struct StateLayout {
 // (profiles/r01_scan_modes.txt; the slower modes 1, 3, 4 and 6 of round 1
 // are recorded in tools/rejected/, not built).
 uint32_t effective_scan_mode(const vbdr_config &n) {
-  const bool fast = n.layout != VBDR_LAYOUT_PACKED;
+  const bool fast = n.layout != VBDR_LAYOUT_PACKED;  // layout S as fast: the block cache
   return n.scan_mode ? n.scan_mode : (fast ? 5u : 2u);
 }
 
@@ -106,7 +107,7 @@ std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *p
     n.seed_a0 = 0x5EED0001u;
     n.seed_a1 = 0x5EED0002u;
   }
-  if (n.layout > 1) return "layout must be 0 (fast) or 1 (packed)";
+  if (n.layout > 2) return "layout must be 0 (fast), 1 (packed) or 2 (stamps)";
   if (n.scan_mode != 0 && n.scan_mode != 2 && n.scan_mode != 5)
     return "scan_mode must be 0 (default), 2 (L2 check) or 5 (block cache + L2 check)";
   if (n.est_lanes > 32 || (n.est_lanes & (n.est_lanes - 1)))
@@ -121,8 +122,8 @@ std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *p
   } else if (n.drv_shard != 0) {
     return "drv_shard needs drv_shards > 1";
   }
-  if (n.estimator == 2 && n.layout != VBDR_LAYOUT_PACKED)
-    return "PCSA needs layout packed (every rank recorded: the sliding bitmap)";
+  if (n.estimator == 2 && n.layout == VBDR_LAYOUT_FAST)
+    return "PCSA needs layout packed or stamps (every rank recorded: the sliding bitmap)";
   if (n.m < 2 || !is_pow2(n.m)) return "m must be a power of two >= 2";
   if (n.k < 1) return "k must be >= 1";
   if (n.n_phys < 4 || !is_pow2(n.n_phys) || n.n_phys > (1ull << 32))
@@ -147,13 +148,15 @@ std::string layout_state(const vbdr_config *c, vbdr_config *norm, StateLayout *p
     return "layout packed needs 2^zbits - 2 >= k (canonical export, R#2)";
   n.zbits = zb;
   n.rank_cap = L;
-  const uint32_t F = 32u / zb;
-  const uint32_t W = (L + F - 1) / F;
+  const bool stamps = n.layout == VBDR_LAYOUT_STAMPS;
+  // layout S: one u32 stamp per (BDR, rank): L "words" of one field each
+  const uint32_t F = stamps ? 1u : 32u / zb;
+  const uint32_t W = stamps ? L : (L + F - 1) / F;
   uint64_t off = 0;
   pl->off_acc = off;
   off = align256(off + 8 * sizeof(uint64_t));  // (S_tot, V_tot) for tick mod 4
   pl->off_sr = off;
-  if (!packed) off = align256(off + 4ull * n.n_phys);
+  if (!packed && !stamps) off = align256(off + 4ull * n.n_phys);
   pl->off_drv = off;
   const uint64_t drv_n = n.drv_shards > 1 ? n.n_phys / n.drv_shards : n.n_phys;
   off = align256(off + 4ull * W * drv_n);
@@ -196,6 +199,8 @@ uint64_t scan_launches(const vbdr *, uint64_t) { return 1; }
 
 int scan_mode(const vbdr *h) {
   const uint32_t m = effective_scan_mode(h->cfg);
+  if (h->stamps)  // the cache keys by (plane, BDR) word index: L * n_phys < 2^32
+    return m == 5 && (uint64_t)h->p.L * h->p.n_phys < (1ull << 32) ? 5 : 2;
   // mode 5 keys its shared-memory cache by word index: fast needs n_phys < 2^32,
   // packed n_phys <= 2^28 (and W <= 15); otherwise use mode 2
   if (m == 5 && (h->fast ? h->p.n_phys >= (1ull << 32) : (h->p.n_phys > (1ull << 28) || h->p.W > 15)))
@@ -249,6 +254,12 @@ void decode_ages(const vbdr *h, WordAt word, int mode, uint16_t *out) {
     if (mode == 1) {
       if (!h->fast) v = (v == sent) ? k : (v ? v - 1u : 0u);
       if (v > k) v = k;
+    }
+    if (h->stamps) {  // age = closed tick - stamp; never stamped: k (canonical) / 0xFFFF
+      const uint32_t st = word(r - 1), closed = h->p.tick - 1u;
+      v = st == 0u ? (mode == 1 ? k : 0xFFFFu) : closed - st;
+      if (mode == 1 && v > k) v = k;
+      if (v > 0xFFFFu) v = 0xFFFFu;
     }
     out[r - 1] = (uint16_t)v;
   }
@@ -339,8 +350,10 @@ vbdr_status after_slide(vbdr_t *h, void *stream) {
   if (h->p.tick >= kTickLimit) {
     // Every stamp is stale after a slide; restart the tick at 4 (kTickLimit
     // mod 4, so the register buffers and accumulator slots keep rotating).
-    if (h->fast) {
-      const cudaError_t m = cudaMemsetAsync(h->p.sr, 0, 4ull * h->p.n_phys, S(stream));
+    if (h->fast || h->stamps) {
+      const cudaError_t m = h->fast ? cudaMemsetAsync(h->p.sr, 0, 4ull * h->p.n_phys, S(stream))
+                                    : cudaMemsetAsync(h->p.drv, 0, 4ull * h->p.W * h->p.n_phys,
+                                                      S(stream));
       if (m != cudaSuccess) return cuda_fail(h, m, "tick wrap");
     }
     h->p.tick = 4;
@@ -402,6 +415,7 @@ vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, v
   }
   cudaGetLastError();  // do not inherit someone else's error
   h->fast = h->cfg.layout == VBDR_LAYOUT_FAST;
+  h->stamps = h->cfg.layout == VBDR_LAYOUT_STAMPS;
   uint8_t *base = static_cast<uint8_t *>(d_state);
   DevParams &p = h->p;
   p.acc = reinterpret_cast<unsigned long long *>(base + pl.off_acc);
@@ -438,7 +452,15 @@ vbdr_status vbdr_create(const vbdr_config *cfg, void *d_state, uint64_t bytes, v
   in.off_drv = pl.off_drv;
   in.off_regmax = pl.off_regmax;
   in.state_bytes = pl.bytes;
-  cudaError_t ce = vbdr_launch::init(p, h->fast, S(stream));
+  cudaError_t ce;
+  if (h->stamps) {  // no DRs to InitDR: every stamp 0 (never recorded)
+    DevParams p0 = p;
+    p0.W = 0;
+    ce = vbdr_launch::init(p0, false, S(stream));
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(p.drv, 0, 4ull * p.W * p.n_phys, S(stream));
+  } else {
+    ce = vbdr_launch::init(p, h->fast, S(stream));
+  }
   if (ce == cudaSuccess)
     ce = cudaMemsetAsync(h->regmax_base + h->regmax_stride, 0, h->cfg.n_phys, S(stream));
   if (ce != cudaSuccess) {
@@ -483,8 +505,10 @@ vbdr_status vbdr_scan_slice(vbdr_t *h, const uint32_t *d_pairs, uint64_t n_pairs
   if (!d_pairs || (reinterpret_cast<uintptr_t>(d_pairs) & 15u))
     return fail(h, VBDR_EINVAL, "d_pairs must be a 16-byte aligned device pointer");
   if (vbdr_status s = check_async(h, "before scan")) return s;
-  const cudaError_t e = vbdr_launch::scan(h->p, h->fast, scan_mode(h), d_pairs, n_pairs,
-                                          S(stream));
+  const cudaError_t e = h->stamps
+                            ? vbdr_launch::scan_stamps(h->p, scan_mode(h), d_pairs, n_pairs, S(stream))
+                            : vbdr_launch::scan(h->p, h->fast, scan_mode(h), d_pairs, n_pairs,
+                                                S(stream));
   if (e != cudaSuccess) return cuda_fail(h, e, "scan launch");
   h->info.launches += scan_launches(h, n_pairs);
   return VBDR_OK;
@@ -500,7 +524,8 @@ vbdr_status vbdr_slide(vbdr_t *h, void *stream) {
   if (h->p.drv_n != h->p.n_phys)
     return fail(h, VBDR_ESTATE, "a register-sharded handle closes slices with slide_delta");
   if (vbdr_status s = check_async(h, "before slide")) return s;
-  const cudaError_t e = vbdr_launch::slide(h->p, h->fast, S(stream));
+  const cudaError_t e = h->stamps ? vbdr_launch::slide_stamps(h->p, S(stream))
+                                 : vbdr_launch::slide(h->p, h->fast, S(stream));
   if (e != cudaSuccess) return cuda_fail(h, e, "slide launch");
   return after_slide(h, stream);
 }
@@ -624,6 +649,7 @@ vbdr_status vbdr_slide_multicast(vbdr_t *h, void *d_mc_state, uint64_t j0, uint6
     return fail(h, VBDR_EINVAL,
                 "need a 256-byte aligned multicast state address and 0 <= j0 < j1 <= n_phys, "
                 "both multiples of 4");
+  if (h->stamps) return fail(h, VBDR_ESTATE, "slide_multicast: layouts fast and packed only");
   if (h->fast ? !drv_covers(h, j0, j1) : h->cfg.drv_shards > 1)
     return fail(h, VBDR_EINVAL, h->fast ? "[j0, j1) outside this handle's DRV shard"
                                         : "layout packed keeps a full DRV replica per rank");
@@ -1000,7 +1026,8 @@ vbdr_status vbdr_scan_slice_host(vbdr_t *h, const uint32_t *h_pairs, uint64_t n_
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_copied[slot], h->copy_stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, h->ev_copied[slot], 0);
     if (e == cudaSuccess) {
-      e = vbdr_launch::scan(h->p, h->fast, scan_mode(h), dst, cnt, cs);
+      e = h->stamps ? vbdr_launch::scan_stamps(h->p, scan_mode(h), dst, cnt, cs)
+                    : vbdr_launch::scan(h->p, h->fast, scan_mode(h), dst, cnt, cs);
       h->info.launches += scan_launches(h, cnt);
     }
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_scanned[slot], cs);

@@ -16,8 +16,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libvbdr.so")  # the in-tree build
 
-LAYOUT_FAST, LAYOUT_PACKED = 0, 1
-LAYOUTS = {"fast": LAYOUT_FAST, "packed": LAYOUT_PACKED}
+LAYOUT_FAST, LAYOUT_PACKED, LAYOUT_STAMPS = 0, 1, 2
+LAYOUTS = {"fast": LAYOUT_FAST, "packed": LAYOUT_PACKED, "stamps": LAYOUT_STAMPS}
 ESTIMATORS = {"hll": 0, "loglog": 1, "pcsa": 2}
 
 STATUS = {0: "ok", -1: "EINVAL", -2: "ERANGE", -3: "ESTATE", -4: "ENOMEM", -5: "ECUDA"}
@@ -198,14 +198,18 @@ class VBDR:
         return {name: getattr(inf, name) for name, _ in vbdr_info_t._fields_}
 
     def sr_view(self):
-        """The stamp words (layout fast) as an int32 tensor view for the
-        multi-GPU max merge: all stamps are < 2^31, so signed MAX is exact."""
+        """The stamp words as an int32 tensor view for the multi-GPU max merge
+        (layout fast: one per BDR; layout stamps: L planes of one per BDR):
+        all stamps are < 2^31, so signed MAX is exact."""
         import torch
         inf = self.info()
-        if self.layout != "fast":
-            raise RuntimeError("only the fast layout has mergeable stamps")
-        off = inf["off_sr"]
-        return self.state[off:off + 4 * self.n_phys].view(torch.int32)
+        if self.layout == "stamps":
+            off, n = inf["off_drv"], 4 * inf["words"] * self.n_phys
+        elif self.layout == "fast":
+            off, n = inf["off_sr"], 4 * self.n_phys
+        else:
+            raise RuntimeError("layout packed has no mergeable stamps (use the NVLS AND merge)")
+        return self.state[off:off + n].view(torch.int32)
 
     def debug_set_tick(self, tick: int):
         """``vbdr_debug_set_tick`` (tests only)."""

@@ -998,3 +998,66 @@ def test_nvls_slide_rejects_bad_ranges():
         pool.slide_multicast(base + 16)  # not 256-byte aligned
     packed = VBDR(32, 4, 1 << 12, layout="packed", device=DEV)
     packed.slide_multicast(packed.state.data_ptr())  # full range: fine
+
+
+@pytest.mark.parametrize("estimator,scan_mode", [("hll", 0), ("hll", 2), ("pcsa", 0),
+                                                 ("loglog", 5)])
+def test_stamps_layout_tiny(estimator, scan_mode):
+    """Layout S (per-(BDR, rank) last-seen stamps) against the
+    oracle's VBDR-gsmall pool (Alg.8 + Alg.9): canonical C_k = min(age, k),
+    registers, pool sums and estimates at every boundary of 12 slices, ragged
+    batches, an empty slice."""
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "gsmall")
+    pool = VBDR(32, 4, 1 << 12, layout="stamps", estimator=estimator, scan_mode=scan_mode,
+                device=DEV)
+    inf = pool.info()
+    assert inf["words"] == cfg.L and inf["fields"] == 1
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    slices = []
+    for t in range(12):
+        pairs = synth.generate(tr, t) if t != 6 else np.zeros((0, 2), np.uint32)
+        slices.append(pairs)
+        for a, b in ((0, 3), (3, 4001), (4001, len(pairs))):
+            if b > a:
+                pool.scan_slice(dev_u32(pairs[a:b]))
+        pool.slide()
+        ref.slice(pairs)
+        assert np.array_equal(pool.export_ages(canonical=True), ref.ck()), "C_k"
+        if estimator == "hll":
+            compare_boundary(pool, ref, [], hosts_np, hosts, np.concatenate(slices[-4:]),
+                             check_ages=False)
+            continue
+        V = ref.readout_pcsa() if estimator == "pcsa" else ref.readout()
+        assert np.array_equal(pool.export_regmax(), V)
+        assert pool.export_pool_sums() == (int(V.astype(np.int64).sum()), int((V == 0).sum()))
+        est = pool.estimate(hosts).cpu().numpy()
+        want = oracle.estimate_variant(V, hosts_np, cfg.b, cfg.z, estimator)
+        check_estimates(est, want, variant_floor(V, hosts_np, cfg.b, cfg.z, estimator))
+
+
+def test_stamps_layout_caida_sampled():
+    """Layout S at the caida pool (2^22 BDRs, 100 planes of stamps = 400 MiB),
+    k + 2 full-size slices: registers = the rebuild from the window's pairs,
+    exact pool sums, sampled hosts' estimates against the oracle."""
+    tr = synth.CONFIGS["caida"]
+    b, k, z = 7, 5, 1 << 22
+    L = 32 - b
+    pool = VBDR(128, k, z, layout="stamps", device=DEV)
+    per_slice = []
+    for t in range(k + 2):
+        pairs = synth.generate(tr, t)
+        pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        per_slice.append(oracle.rebuild(pairs, b, L, z, 0x5EED0001, 0x5EED0002))
+    M = per_slice[-k]
+    for x in per_slice[-k + 1:]:
+        M = np.maximum(M, x)
+    assert np.array_equal(pool.export_regmax(), M)
+    assert pool.export_pool_sums() == oracle_pool_sums(M, L)
+    hosts = tr.host_ids()[:: 997]
+    est = pool.estimate(dev_u32(hosts)).cpu().numpy()
+    want = oracle.estimate_M(M, hosts, b, z)
+    assert np.allclose(est, want, rtol=1e-9, atol=1e-9 * np.abs(want).max())
