@@ -584,9 +584,7 @@ def merge_stamps_tensor(sr, group=None):
     commutative and idempotent, so any split of a slice's pairs over ranks gives
     the same merged stamps."""
     import torch.distributed as dist
-    if group is None and (not dist.is_available() or not dist.is_initialized()):
-        return sr
-    if dist.get_world_size(group) <= 1:
+    if not dist.is_available() or not dist.is_initialized():
         return sr
     dist.all_reduce(sr, op=dist.ReduceOp.MAX, group=group)
     return sr
@@ -713,10 +711,12 @@ def slide_merged(pool: "VBDR", group=None, mode: str = "sharded", delta=None, sh
     sparse : as sharded, but the ranks exchange only the BDRs their pairs
              touched (vbdr_sparse_extract, all-to-all of u32 records,
              vbdr_sparse_apply): for pools far sparser than a slice.
-    With one rank this is vbdr_slide."""
+    Without an initialised process group this is vbdr_slide; a group of one
+    still runs the collectives (the N = 1 point of a scaling run, and the
+    NCCL calls' test on a one-GPU box: tests/test_gpu_dist.py)."""
     import torch.distributed as dist
     world, rank = _world(group)
-    if world <= 1:
+    if not dist.is_available() or not dist.is_initialized():
         pool.slide()
         return
     if mode == "stamps":
@@ -793,7 +793,7 @@ class SparseMerge:
                                                   C.c_void_p(self.counts.data_ptr()),
                                                   _stream_ptr(None)), "vbdr_sparse_extract")
         want = torch.tensor([int(self.counts.max())], dtype=torch.int64, device=self.pool.device)
-        if self.world > 1:
+        if dist.is_available() and dist.is_initialized():
             dist.all_reduce(want, op=dist.ReduceOp.MAX, group=self.group)
         cap = max(1024, int(int(want) * self.headroom + 1023) // 1024 * 1024)
         self._alloc(cap)

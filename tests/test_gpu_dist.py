@@ -24,10 +24,11 @@ def _port():
         return s.getsockname()[1]
 
 
-def _torchrun(n, *args):
+def _torchrun(n, *args, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", f"--master-port={_port()}", *args]
-    return subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    return subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+                          env={**os.environ, **(env or {})})
 
 
 @pytest.mark.parametrize("mode", ["stamps", "delta", "sharded", "sparse", "sharded-state"])
@@ -36,6 +37,19 @@ def test_slide_merged_multi_rank(mode, world):
     r = _torchrun(world, os.path.join("tests", "dist_worker.py"), mode)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert f"parity=ok" in r.stdout
+
+
+@pytest.mark.parametrize("mode", ["stamps", "delta", "sharded", "sparse", "sharded-state", "p2p"])
+def test_slide_merged_nccl_group_of_one(mode):
+    """Every merge through the NCCL backend (all_reduce MAX on u32 / u8,
+    reduce_scatter_tensor MAX, all_gather_into_tensor, all_to_all_single, SUM
+    of the pool sums) and PeerMerge's symmetric-memory rendezvous and device
+    barriers, on the device tensors, with a group of one: oracle parity at
+    every boundary.  (One GPU per box: more NCCL ranks need more GPUs.)"""
+    r = _torchrun(1, os.path.join("tests", "dist_worker.py"), mode,
+                  env={"VBDR_TEST_BACKEND": "nccl"})
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "parity=ok" in r.stdout
 
 
 @pytest.mark.parametrize("merge", ["sharded", "sparse"])

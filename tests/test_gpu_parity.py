@@ -812,7 +812,7 @@ def test_plan_estimate_caida_full_size(kind):
 @pytest.mark.parametrize("kind", ["sorted", "staged"])
 @pytest.mark.parametrize("g,z_log2,n_hosts", [(64, 12, 1001), (16, 12, 3),
                                                (32, 20, 7 * 512 * 148 - 5), (2, 7, 33),
-                                               (256, 24, 300_001)])
+                                               (256, 24, 300_001), (128, 22, 1_200_001)])
 def test_plan_accumulator_modes_and_ragged_hosts(g, z_log2, n_hosts, kind):
     """Plan rounds for a host list with duplicates and a ragged tail, for 3
     hosts (almost every round is padding) and for the largest host count a
