@@ -6,12 +6,12 @@
 // register array is small (n_phys <= 2^22, 4 MiB) the same sums can be formed
 // from shared memory instead:
 //   * a PLAN, built once per host list, assigns every host to an accumulator
-//     slot of one warp of one of `ctas` persistent CTAs, spreading hosts over
-//     CTAs first, then warps, then lanes (slot_host below), and lists, for
-//     every (CTA, register block of 2^16) phase and every warp, the warp's
-//     (host, i) gathers that fall in that block (Alg.5 / Alg.3 indices,
-//     precomputed) as ROUNDS of 32 entries (offset in block | accumulator
-//     byte offset << 16), one entry per lane.  Any lane may serve any of its
+//     slot of one warp of one of P persistent CTAs, spreading hosts over
+//     CTAs first, then warps, then lanes (host_of below), and lists, for
+//     every (CTA, register block) phase and every warp, the warp's (host, i)
+//     gathers that fall in that block (Alg.5 / Alg.3 indices, precomputed) as
+//     ROUNDS of 32 entries (offset in block | accumulator byte offset << 16),
+//     one entry per lane.  Any lane may serve any of its
 //     warp's hosts, so all lanes stay busy (a thread-owns-its-hosts layout
 //     idles ~35 % of the lanes on the longest run).  The entries of a group
 //     are first striped over its rounds by shared-memory bank of their
@@ -27,6 +27,9 @@
 //     zero count for M = 0 (S = S' + V 2^L; S' <= g 2^(L-1) = 2^31 for
 //     L = 32 - log2 g) -- no L2 gathers.  The last step is the fp64 finish
 //     of k_estimate.
+// (Splitting the grid into host groups x register ranges, so each CTA
+// streams only part of the array, measured slower: the register stream is
+// not the bound; tools/rejected/plan_ranges, profiles/r02_plan_ranges.txt.)
 // Integer sums make the result bit-identical to the gather kernel.
 #include "vbdr_dev.cuh"
 
@@ -48,10 +51,9 @@ namespace {
 
 constexpr int kT = vbdr_launch::kPlanThreads;   // 512
 constexpr int kW = kT / 32;                     // 16 warps
-constexpr int kSlots = vbdr_launch::kPlanSlots; // 7
 constexpr int kCap = vbdr_launch::kPlanEntCap;  // entries per (CTA, phase) buffer
 constexpr int kStride = vbdr_launch::kPlanStride;  // round starts per key (kW + 1 used)
-constexpr int kAccW = kSlots * 32 + 32;         // per warp: host slots + one trash word per lane
+// per warp: `slots` host slots per lane + one trash word per lane (accw words)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -61,19 +63,21 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 struct BuildArgs {
   const uint32_t *hosts;
   uint64_t n;
-  uint32_t g, A0, mask, block_log2, phases, ctas;
-  uint32_t *counts;      // [ctas * phases * kW * 32]: per (group, bank) counts, then cursors
-  uint32_t *starts;      // [ctas * phases * kStride]: round offsets of the kW warps of a key
-  uint32_t *range_base;  // [ctas * phases + 1], in entries
+  uint32_t g, A0, mask, block_log2;
+  uint32_t phases;       // register blocks
+  uint32_t P, slots;     // CTAs, accumulator slots per lane
+  uint32_t *counts;      // [P * phases * kW * 32]: per (group, bank) counts, then cursors
+  uint32_t *starts;      // [P * phases * kStride]: round offsets of the kW warps of a key
+  uint32_t *range_base;  // [P * phases + 1], in entries
   uint32_t *entries;
   uint32_t *max_range;   // scalar
 };
 
-// Host h -> CTA h % ctas; q = h / ctas -> warp q % 16, lane (q / 16) % 32,
-// slot q / 512: short host lists still use every CTA and warp.
-__host__ __device__ __forceinline__ uint64_t slot_host(uint32_t cta, uint32_t warp, uint32_t lane,
-                                                       uint32_t slot, uint32_t ctas) {
-  return ((uint64_t)slot * kT + lane * kW + warp) * ctas + cta;
+// Host h -> CTA p = h % P; q = h / P -> warp q % 16, lane (q / 16) % 32,
+// slot q / 512: short host lists still use every CTA and warp.  The host's
+// accumulator index in its warp is slot * 32 + lane.
+__host__ __device__ __forceinline__ uint64_t host_of(uint32_t p, uint64_t q, uint32_t P) {
+  return q * P + p;
 }
 
 // (host, i) -> key = (CTA, phase), warp, bank of the register in the block,
@@ -81,16 +85,16 @@ __host__ __device__ __forceinline__ uint64_t slot_host(uint32_t cta, uint32_t wa
 __device__ __forceinline__ void locate_entry(const BuildArgs &a, uint64_t h, uint32_t i,
                                              uint64_t &key, uint32_t &warp, uint32_t &bank,
                                              uint32_t &val) {
-  const uint32_t cta = (uint32_t)(h % a.ctas);
-  const uint64_t q = h / a.ctas;
+  const uint32_t p = (uint32_t)(h % a.P);
+  const uint64_t q = h / a.P;
   warp = (uint32_t)(q % kW);
   const uint32_t lane = (uint32_t)((q / kW) % 32u);
   const uint32_t slot = (uint32_t)(q / kT);
   const uint32_t s1 = fmix32(i ^ a.A0);                            // Alg.3
   const uint32_t pidx = fmix32(__ldg(a.hosts + h) ^ s1) & a.mask;  // Alg.3
-  const uint32_t phase = pidx >> a.block_log2;
+  const uint32_t blk = pidx >> a.block_log2;
   const uint32_t off = pidx & ((1u << a.block_log2) - 1u);
-  key = (uint64_t)cta * a.phases + phase;
+  key = (uint64_t)p * a.phases + blk;
 #if VBDR_PLAN_SORT == 1
   bank = lane;  // accumulator bank
 #elif VBDR_PLAN_SORT == 2
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(kT) k_plan_pad(BuildArgs a) {
   const uint32_t r0 = a.starts[key * kStride + w], R = a.starts[key * kStride + w + 1] - r0;
   for (uint32_t i = n_w + lane; i < 32u * R; i += 32u) {
     const uint32_t pos = stripe(i, R);
-    a.entries[a.range_base[key] + 32u * r0 + pos] = (uint32_t)(kSlots * 32 + (pos & 31u)) << 18;
+    a.entries[a.range_base[key] + 32u * r0 + pos] = (a.slots * 32u + (pos & 31u)) << 18;
   }
 }
 
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(kT) k_plan_sched(BuildArgs a, const uint32_t *
   const uint32_t r0 = a.starts[key * kStride + w], R = a.starts[key * kStride + w + 1] - r0;
   uint32_t *L = E + 32u * r0;  // this warp's list
   uint32_t *out = ent + 32u * r0;
-  constexpr uint32_t kTrash = (uint32_t)kSlots * 32u;  // accumulator indices >= this are padding
+  const uint32_t kTrash = a.slots * 32u;  // accumulator indices >= this are padding
   constexpr uint32_t kTaken = 0xFFFFFFFFu;
   // drop the padding: compact the real entries to the front
   uint32_t rem = 0;
@@ -320,12 +324,13 @@ struct __align__(128) PlanSmem {
   uint8_t tab[2][1 << BLOCK_LOG2];
   uint32_t ent[2][kCap];
   uint32_t start[2][kStride];
-  // per warp: [0, kAccW) S' = sum over M >= 1 of 2^(L - M) (HLL) or M;
-  // [kAccW, 2 kAccW) the zero count, V 2^L (HLL, mod 2^32) or V
-  uint32_t acc[kW][2 * kAccW];
   uint64_t full[2];          // TMA bytes of buffer b landed
   uint64_t empty[2];         // all kW consumer warps are done with buffer b
   double etot_z;
+  uint32_t ok;               // cleared if a staged transfer never landed
+  // followed by the accumulators, per warp 2 accw u32 (dynamic):
+  // [0, accw) S' = sum over M >= 1 of 2^(L - M) (HLL) or M;
+  // [accw, 2 accw) V, the number of M = 0 registers
 };
 
 __device__ __forceinline__ bool mbar_wait(uint64_t *bar, uint32_t parity) {
@@ -341,6 +346,39 @@ __device__ __forceinline__ bool mbar_wait(uint64_t *bar, uint32_t parity) {
   return true;
 }
 
+// One host's fp64 finish from its integer sums (k_estimate's operation order).
+template <bool SUMS>
+__device__ __forceinline__ void plan_finish(const EstParams &e, uint64_t h, uint32_t Sp, uint32_t V,
+                                            bool HLL, double etot_z, double *out,
+                                            unsigned long long *outS, uint32_t *outV) {
+  const unsigned long long S = Sp + (HLL ? (unsigned long long)V << e.L : 0ull);
+  if constexpr (SUMS) {
+    outS[h] = S;
+    outV[h] = V;
+  } else {
+    const double g = (double)e.g;
+    double Es;
+    if (e.est == 0u) {
+      Es = hll_finish(e.agg, __dmul_rn((double)S, e.inv2L), e.lc_g, V, g);
+    } else {
+      Es = __dmul_rn(e.coef_g, exp2(__ddiv_rn((double)S, g)));
+    }
+    const double est = __dmul_rn(e.C, __dsub_rn(__ddiv_rn(Es, g), etot_z));
+    out[h] = est > 0.0 ? est : 0.0;
+  }
+}
+
+template <bool SUMS>
+__device__ __forceinline__ void plan_poison(uint64_t h, double *out, unsigned long long *outS,
+                                            uint32_t *outV) {
+  if constexpr (SUMS) {  // loud: never a stale value from an earlier slice
+    outS[h] = ~0ull;
+    outV[h] = ~0u;
+  } else {
+    out[h] = __longlong_as_double(0x7FF8000000000000ll);  // NaN
+  }
+}
+
 // kW consumer warps + one producer warp (TMA issue only).  Buffers are
 // handed over with full / empty mbarriers, so a warp that finishes a block
 // early starts on the next one instead of waiting at a CTA barrier.
@@ -354,12 +392,12 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
   pdl_wait();
   extern __shared__ __align__(128) uint8_t raw[];
   PlanSmem<BLOCK_LOG2> &sm = *reinterpret_cast<PlanSmem<BLOCK_LOG2> *>(raw);
+  const uint32_t accw = pl.st_slots * 32u + 32u;
+  uint32_t *acc_all = reinterpret_cast<uint32_t *>(raw + sizeof(PlanSmem<BLOCK_LOG2>));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t P = gridDim.x, p = blockIdx.x;
   if (w < kW) {
-    for (int i = lane; i < kAccW; i += 32) {
-      sm.acc[w][i] = 0u;
-      sm.acc[w][kAccW + i] = 0u;
-    }
+    for (uint32_t i = lane; i < 2u * accw; i += 32u) acc_all[w * 2u * accw + i] = 0u;
   }
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
@@ -367,6 +405,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
       asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(&sm.empty[b])), "r"(kW));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    sm.ok = 1u;
     if (!SUMS) {
       const unsigned long long St = e.acc[0], Vt = e.acc[1];
       double Et;
@@ -380,6 +419,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
   }
   __syncthreads();
   const uint32_t phases = pl.phases;
+  const uint8_t *regs = e.regmax;
   if (w == kW) {  // producer
     if (lane == 0) {
       for (uint32_t ph = 0; ph < phases; ++ph) {
@@ -387,9 +427,9 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
         // buffer b last held phase ph - 2: wait for its (ph/2 - 1)-th release
         if (ph >= 2 && !mbar_wait(&sm.empty[b], ((ph >> 1) + 1u) & 1u)) {
           atomicAdd(err, 1ull);
-          return;
+          break;
         }
-        const uint64_t key = (uint64_t)blockIdx.x * phases + ph;
+        const uint64_t key = (uint64_t)p * phases + ph;
         const uint32_t e0 = pl.range_base[key], e1 = pl.range_base[key + 1];
         const uint32_t ebytes = (e1 - e0) * 4u;  // ranges are multiples of 32 entries
         const uint32_t sbytes = kStride * 4u;
@@ -404,7 +444,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
               "l"(src), "r"(bytes), "r"(fb)
               : "memory");
         };
-        bulk(sm.tab[b], e.regmax + (uint64_t)ph * BLOCK, BLOCK);
+        bulk(sm.tab[b], regs + (uint64_t)ph * BLOCK, BLOCK);
         if (ebytes) bulk(sm.ent[b], pl.entries + e0, ebytes);
         bulk(sm.start[b], pl.starts + key * kStride, sbytes);
 #if VBDR_PLAN_PREFETCH
@@ -412,14 +452,14 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
         // stage refill then waits on L2, not DRAM, latency
         const uint32_t pf = ph + VBDR_PLAN_PREFETCH;
         if (pf < phases) {
-          const uint64_t k2 = (uint64_t)blockIdx.x * phases + pf;
+          const uint64_t k2 = (uint64_t)p * phases + pf;
           const uint32_t f0 = pl.range_base[k2], f1 = pl.range_base[k2 + 1];
           if (f1 > f0)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pl.entries + f0),
                          "r"((f1 - f0) * 4u)
                          : "memory");
 #if VBDR_PLAN_PREFETCH_TAB
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(e.regmax + (uint64_t)pf * BLOCK),
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(regs + (uint64_t)pf * BLOCK),
                        "r"(BLOCK)
                        : "memory");
 #endif
@@ -427,90 +467,72 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
 #endif
       }
     }
-    return;
-  }
-  uint32_t *acc = sm.acc[w];
-  uint32_t *accv = acc + kAccW;
-  const uint32_t acc_base = smem_u32(acc);
-  const uint32_t K = 1u << e.L;  // 2^(L - M) = K >> M
-  bool ok = true;  // a staged transfer that never lands poisons this warp's hosts (NaN)
-  for (uint32_t ph = 0; ph < phases; ++ph) {
-    const int b = ph & 1;
-    if (!mbar_wait(&sm.full[b], (ph >> 1) & 1u)) {
-      if (lane == 0) atomicAdd(err, 1ull);
-      ok = false;
-      break;
-    }
-    const uint8_t *tab = sm.tab[b];
-    const uint32_t r0 = sm.start[b][w], r1 = sm.start[b][w + 1];
-    const uint32_t *ent = sm.ent[b] + lane;
-    // one entry per lane per round; ILP rounds' loads are issued before their
-    // atomics (one atomic per lane: the zero count or S', same bank either way)
-    // one atomic per lane: M >= 1 adds its term to S', M = 0 adds to the
-    // zero count (2^L for HLL, so both are one shift; same bank either way)
-    auto add = [&](uint32_t v, uint32_t M) {
-      const uint32_t c = HLL ? K >> M : (M == 0u ? 1u : M);
-      const uint32_t addr = acc_base + (v >> 16) + (M == 0u ? 4u * kAccW : 0u);
-      asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(c) : "memory");
-    };
-    uint32_t r = r0;
-    for (; r + ILP <= r1; r += ILP) {
-      uint32_t v[ILP], M[ILP];
-#pragma unroll
-      for (int j = 0; j < ILP; ++j) v[j] = ent[(r + j) * 32u];
-#pragma unroll
-      for (int j = 0; j < ILP; ++j) M[j] = tab[v[j] & (BLOCK - 1u)];
-#pragma unroll
-      for (int j = 0; j < ILP; ++j) add(v[j], M[j]);
-    }
-    for (; r < r1; ++r) {
-      const uint32_t v = ent[r * 32u];
-      add(v, tab[v & (BLOCK - 1u)]);
-    }
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(&sm.empty[b])) : "memory");
-  }
-  pdl_trigger();
-  const double g = (double)e.g;
-#pragma unroll
-  for (int s = 0; s < kSlots; ++s) {
-    const uint64_t h = slot_host(blockIdx.x, w, lane, s, gridDim.x);
-    // (a warp that timed out still writes its hosts: NaN below)
-    if (h >= n) break;
-    const uint32_t Sp = acc[s * 32 + lane], Vz = accv[s * 32 + lane];
-    // HLL: Vz = V 2^L mod 2^32, which wraps only for V = g when g 2^L = 2^32,
-    // i.e. every register zero -- exactly when S' = 0 (each M >= 1 adds >= 1)
-    const uint32_t V = HLL ? (Sp == 0u ? e.g : Vz >> e.L) : Vz;
-    const unsigned long long S = Sp + (HLL ? (unsigned long long)V << e.L : 0ull);
-    if (!ok) {  // loud: never a stale value from an earlier slice
-      if constexpr (SUMS) {
-        outS[h] = ~0ull;
-        outV[h] = ~0u;
-      } else {
-        out[h] = __longlong_as_double(0x7FF8000000000000ll);  // NaN
+  } else {
+    uint32_t *acc = acc_all + w * 2u * accw;
+    const uint32_t acc_base = smem_u32(acc);
+    const uint32_t vofs = 4u * accw;  // V array, same bank as the host's S'
+    const uint32_t K = 1u << e.L;     // 2^(L - M) = K >> M
+    for (uint32_t ph = 0; ph < phases; ++ph) {
+      const int b = ph & 1;
+      if (!mbar_wait(&sm.full[b], (ph >> 1) & 1u)) {
+        if (lane == 0) {
+          atomicAdd(err, 1ull);
+          sm.ok = 0u;  // a staged transfer that never landed poisons the CTA's hosts (NaN)
+        }
+        break;
       }
+      const uint8_t *tab = sm.tab[b];
+      const uint32_t r0 = sm.start[b][w], r1 = sm.start[b][w + 1];
+      const uint32_t *ent = sm.ent[b] + lane;
+      // one entry per lane per round; ILP rounds' loads are issued before their
+      // atomics.  One atomic per lane: M >= 1 adds its term to S', M = 0 adds
+      // 1 to V
+      auto add = [&](uint32_t v, uint32_t M) {
+        const uint32_t cv = M == 0u ? 1u : (HLL ? K >> M : M);
+        const uint32_t addr = acc_base + (v >> 16) + (M == 0u ? vofs : 0u);
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(cv) : "memory");
+      };
+      uint32_t r = r0;
+      for (; r + ILP <= r1; r += ILP) {
+        uint32_t v[ILP], M[ILP];
+#pragma unroll
+        for (int j = 0; j < ILP; ++j) v[j] = ent[(r + j) * 32u];
+#pragma unroll
+        for (int j = 0; j < ILP; ++j) M[j] = tab[v[j] & (BLOCK - 1u)];
+#pragma unroll
+        for (int j = 0; j < ILP; ++j) add(v[j], M[j]);
+      }
+      for (; r < r1; ++r) {
+        const uint32_t v = ent[r * 32u];
+        add(v, tab[v & (BLOCK - 1u)]);
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(&sm.empty[b])) : "memory");
+    }
+  }
+  __syncthreads();
+  pdl_trigger();
+  const double etot_z = SUMS ? 0.0 : sm.etot_z;
+  // accumulator index (slot, lane) of warp w <-> q = slot 512 + lane 16 + w
+  const uint32_t qn = pl.st_slots * (uint32_t)kT;
+  for (uint32_t q = tid; q < qn; q += blockDim.x) {
+    const uint64_t h = host_of(p, q, P);
+    if (h >= n) continue;  // (a CTA that timed out still writes its hosts: NaN)
+    const uint32_t ww = q % kW, ll = (q / kW) % 32u, ss = q / kT;
+    const uint32_t *acc = acc_all + ww * 2u * accw;
+    if (!sm.ok) {
+      plan_poison<SUMS>(h, out, outS, outV);
       continue;
     }
-    if constexpr (SUMS) {
-      outS[h] = S;
-      outV[h] = V;
-    } else {
-      double Es;
-      if (e.est == 0u) {
-        Es = hll_finish(e.agg, __dmul_rn((double)S, e.inv2L), e.lc_g, V, g);
-      } else {
-        Es = __dmul_rn(e.coef_g, exp2(__ddiv_rn((double)S, g)));
-      }
-      const double est = __dmul_rn(e.C, __dsub_rn(__ddiv_rn(Es, g), sm.etot_z));
-      out[h] = est > 0.0 ? est : 0.0;
-    }
+    plan_finish<SUMS>(e, h, acc[ss * 32u + ll], acc[accw + ss * 32u + ll], HLL, etot_z, out, outS,
+                      outV);
   }
 }
 
 template <int BL>
 cudaError_t launch_est(const EstParams &e, const PlanLayout &pl, uint64_t n, double *out,
                        unsigned long long *outS, uint32_t *outV, cudaStream_t s) {
-  const size_t smem = sizeof(PlanSmem<BL>);
+  const size_t smem = vbdr_launch::plan_smem_bytes(pl.block_log2, pl.st_slots);
   auto kern = outS ? (e.est == 0u ? k_estimate_plan<BL, true, true> : k_estimate_plan<BL, true, false>)
                    : (e.est == 0u ? k_estimate_plan<BL, false, true> : k_estimate_plan<BL, false, false>);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -521,6 +543,21 @@ cudaError_t launch_est(const EstParams &e, const PlanLayout &pl, uint64_t n, dou
 }  // namespace
 
 namespace vbdr_launch {
+
+size_t plan_smem_bytes(uint32_t block_log2, uint32_t slots) {
+  size_t fixed = 0;
+  switch (block_log2) {
+#define VBDR_PLAN_SMEM_CASE(BL) \
+  case BL: fixed = sizeof(PlanSmem<BL>); break;
+    VBDR_PLAN_SMEM_CASE(16) VBDR_PLAN_SMEM_CASE(15) VBDR_PLAN_SMEM_CASE(14)
+    VBDR_PLAN_SMEM_CASE(13) VBDR_PLAN_SMEM_CASE(12) VBDR_PLAN_SMEM_CASE(11)
+    VBDR_PLAN_SMEM_CASE(10) VBDR_PLAN_SMEM_CASE(9) VBDR_PLAN_SMEM_CASE(8)
+    VBDR_PLAN_SMEM_CASE(7) VBDR_PLAN_SMEM_CASE(6)
+#undef VBDR_PLAN_SMEM_CASE
+    default: return 0;
+  }
+  return fixed + (size_t)kW * 2u * (slots * 32u + 32u) * 4u;
+}
 
 cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, uint32_t g,
                        uint32_t A0, uint32_t mask, uint32_t *range_size_scratch,
@@ -533,7 +570,8 @@ cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, 
   a.mask = mask;
   a.block_log2 = pl.block_log2;
   a.phases = pl.phases;
-  a.ctas = pl.ctas;
+  a.P = pl.ctas;
+  a.slots = pl.st_slots;
   a.counts = pl.counts;
   a.starts = pl.starts;
   a.range_base = pl.range_base;

@@ -200,7 +200,6 @@ struct EstParams {
 // Plan-based estimate (k_plan.cu): a host list preprocessed into per-(CTA,
 // register block, warp) rounds of 32 entries.  Layout of the caller's plan buffer.
 constexpr int kPlanThreads = 512;
-constexpr int kPlanSlots = 7;     // hosts per thread (accumulator slots per lane)
 constexpr int kPlanEntCap = 8192; // entries per (CTA, block) staged in shared memory
 constexpr int kPlanStride = 20;   // round starts per (CTA, block): 16 warps + total, 16-byte padded
 // Sorted plan (k_splan.cu): entries sorted by register line, P host groups x
@@ -228,6 +227,7 @@ struct PlanLayout {
   uint32_t *entries;
   uint32_t *max_range;   // build: largest (CTA, block) entry count
   unsigned long long *error;  // estimate: set if a staged transfer never landed
+  uint32_t st_slots;     // kind 0: accumulator slots per lane (hosts per thread)
   // kind 2 (sorted plan); counts = bucket cursors, range_size = segment totals
   uint32_t sp_C;           // register ranges per host group
   uint32_t sp_hpg;         // accumulator slots per group (hosts / P, rounded up)
@@ -239,6 +239,7 @@ struct PlanLayout {
   unsigned long long *sp_part;  // [ctas * hpg] partial (S', V) (C > 1)
   uint32_t *sp_gcount;     // [P] arrivals per group (C > 1)
 };
+size_t plan_smem_bytes(uint32_t block_log2, uint32_t slots);  // 0: unsupported block
 cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, uint32_t g,
                        uint32_t A0, uint32_t mask, uint32_t *range_size_scratch, cudaStream_t s);
 cudaError_t estimate_plan(const EstParams &e, const PlanLayout &pl, uint64_t n, double *out,

@@ -265,10 +265,12 @@ void decode_ages(const vbdr *h, WordAt word, int mode, uint16_t *out) {
   }
 }
 
-// Plan geometry for this pool: blocks of up to 2^16 registers (64 KB in shared
-// memory), one persistent CTA per SM.
+// Plan geometry for this pool: one persistent CTA per SM, blocks of up to
+// 2^16 registers (64 KB in shared memory): the largest block whose stages and
+// accumulators (hosts / SMs per CTA) fit shared memory and whose expected
+// entries per (CTA, block) stay well inside a stage.
 struct PlanGeom {
-  uint32_t ctas, phases, block_log2;
+  uint32_t ctas, phases, block_log2, slots;
   uint64_t nkeys, off_range_base, off_starts, off_counts, off_range_size, off_misc, off_entries,
       bytes;
 };
@@ -276,19 +278,35 @@ struct PlanGeom {
 bool plan_geom(const vbdr *h, uint64_t n_hosts, PlanGeom *g) {
   const uint64_t z = h->p.n_phys;
   if (z < 64 || z > (1ull << 22)) return false;  // the array streams through shared memory
-  int sms = 0, dev = 0;
+  int sms = 0, dev = 0, smem_max = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (sms <= 0) sms = 148;
-  const uint64_t T = (uint64_t)sms * vbdr_launch::kPlanThreads;
-  if (n_hosts == 0 || n_hosts > T * vbdr_launch::kPlanSlots) return false;
+  if (smem_max <= 0) smem_max = 232448;
+  if (n_hosts == 0 || n_hosts > 0xFFFFFFFFull) return false;
   // per-host S' (registers with M >= 1) accumulates in a u32 in shared memory:
   // at most g * 2^(L-1) (HLL) or g * 255
   const uint64_t smax =
       (uint64_t)h->cfg.m * (h->cfg.estimator == 0 ? 1ull << (h->p.L - 1) : 255ull);
   if (smax >> 32) return false;
+  const uint64_t hpc = (n_hosts + sms - 1) / sms;
+  const uint64_t slots = (hpc + vbdr_launch::kPlanThreads - 1) / vbdr_launch::kPlanThreads;
+  // accumulator indices travel in the top 14 bits of an entry (<< 18)
+  if (slots * 32 + 32 > (1u << 14)) return false;
+  const double per_key_all = (double)n_hosts * h->cfg.m / sms;  // entries per CTA
+  bool found = false;
+  for (uint32_t bl = z >= (1ull << 16) ? 16u : (uint32_t)log2u(z); bl >= 6 && !found; --bl) {
+    const double per_key = per_key_all / (double)(z >> bl);
+    if (per_key + 6.0 * sqrt(per_key) + 16.0 * 32.0 > (double)vbdr_launch::kPlanEntCap) continue;
+    const size_t smem = vbdr_launch::plan_smem_bytes(bl, (uint32_t)slots);
+    if (smem == 0 || smem > (size_t)smem_max) continue;
+    g->block_log2 = bl;
+    found = true;
+  }
+  if (!found) return false;
   g->ctas = (uint32_t)sms;
-  g->block_log2 = z >= (1ull << 16) ? 16u : (uint32_t)log2u(z);
+  g->slots = (uint32_t)slots;
   g->phases = (uint32_t)(z >> g->block_log2);
   g->nkeys = (uint64_t)g->ctas * g->phases;
   uint64_t off = 0;
@@ -322,6 +340,7 @@ vbdr_launch::PlanLayout plan_layout(const PlanGeom &g, void *d_plan, uint64_t n_
   pl.range_size = reinterpret_cast<uint32_t *>(b + g.off_range_size);
   pl.max_range = reinterpret_cast<uint32_t *>(b + g.off_misc);
   pl.error = reinterpret_cast<unsigned long long *>(b + g.off_misc + 8);
+  pl.st_slots = g.slots;
   pl.entries = reinterpret_cast<uint32_t *>(b + g.off_entries);
   return pl;
 }
