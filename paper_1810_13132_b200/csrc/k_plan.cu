@@ -51,7 +51,7 @@ namespace {
 
 constexpr int kT = vbdr_launch::kPlanThreads;   // 512
 constexpr int kW = kT / 32;                     // 16 warps
-constexpr int kCap = vbdr_launch::kPlanEntCap;  // entries per (CTA, phase) buffer
+constexpr int kCap = vbdr_launch::kPlanEntCap;  // largest entries per (CTA, phase) buffer
 constexpr int kStride = vbdr_launch::kPlanStride;  // round starts per key (kW + 1 used)
 // per warp: `slots` host slots per lane + one trash word per lane (accw words)
 
@@ -292,8 +292,18 @@ __global__ void __launch_bounds__(kT) k_plan_sched(BuildArgs a, const uint32_t *
         __syncwarp();
       }
     }
-    // pad the round; lane j's padding uses lane j's trash accumulator
-    if (lane >= taken) mine = (kTrash + lane) << 18;
+    // pad the round without adding a bank conflict: the padding reads the
+    // register word of the round's first entry (a broadcast) and adds into
+    // trash accumulators on the banks no real entry of the round uses
+    {
+      const bool real = lane < taken;
+      const uint32_t used = __reduce_or_sync(0xffffffffu, real ? 1u << ((mine >> 18) & 31u) : 0u);
+      const uint32_t off0 = __shfl_sync(0xffffffffu, mine, 0) & 0xFFFFu;
+      if (!real) {
+        const uint32_t bank = __fns(~used, 0, (int)(lane - taken) + 1);  // (lane - taken)-th free bank
+        mine = (taken ? off0 : 0u) | ((kTrash + (bank & 31u)) << 18);
+      }
+    }
     out[32u * r + lane] = mine;
     // drop the taken entries from the list
     uint32_t n2 = 0;
@@ -322,7 +332,7 @@ __device__ __forceinline__ double hll_finish(double agg, double D, double lc, ui
 template <int BLOCK_LOG2>
 struct __align__(128) PlanSmem {
   uint8_t tab[2][1 << BLOCK_LOG2];
-  uint32_t ent[2][kCap];
+  uint32_t ent[2][vbdr_launch::plan_ent_cap(BLOCK_LOG2)];
   uint32_t start[2][kStride];
   uint64_t full[2];          // TMA bytes of buffer b landed
   uint64_t empty[2];         // all kW consumer warps are done with buffer b

@@ -298,7 +298,7 @@ bool plan_geom(const vbdr *h, uint64_t n_hosts, PlanGeom *g) {
   bool found = false;
   for (uint32_t bl = z >= (1ull << 16) ? 16u : (uint32_t)log2u(z); bl >= 6 && !found; --bl) {
     const double per_key = per_key_all / (double)(z >> bl);
-    if (per_key + 6.0 * sqrt(per_key) + 16.0 * 32.0 > (double)vbdr_launch::kPlanEntCap) continue;
+    if (per_key + 6.0 * sqrt(per_key) + 16.0 * 32.0 > (double)vbdr_launch::plan_ent_cap(bl)) continue;
     const size_t smem = vbdr_launch::plan_smem_bytes(bl, (uint32_t)slots);
     if (smem == 0 || smem > (size_t)smem_max) continue;
     g->block_log2 = bl;
@@ -901,7 +901,7 @@ vbdr_status vbdr_plan_build_kind(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e != cudaSuccess) return cuda_fail(h, e, "plan_build");
   h->info.launches += 6;
-  if (max_range > (uint32_t)vbdr_launch::kPlanEntCap) {
+  if (max_range > vbdr_launch::plan_ent_cap(pl.block_log2)) {
     h->plans.erase(d_plan);
     return fail(h, VBDR_ERANGE, "a register block holds more entries than shared memory stages");
   }
