@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Summarise ncu output for profiles/ (run here, on the CPU box).
 
-usage: ncu_summary.py launches <launches.csv>          per-kernel launch times + step share
+usage: ncu_summary.py launches <launches.csv> [k1,k2]  per-kernel launch times + step share
+                                                       (over the kernels named, default every
+                                                       k_scan / k_slide / k_estimate*)
        ncu_summary.py full <report.ncu-rep> [label]    key metrics per profiled kernel
        ncu_summary.py traffic <report.ncu-rep> <key>   dram bytes per launch (json fragment)
 """
@@ -32,7 +34,7 @@ def short(name: str) -> str:
     return base.replace("void ", "").replace("<unnamed>::", "")
 
 
-def launches(path):
+def launches(path, only=None):
     rows = list(csv.reader(open(path)))
     h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[h]
@@ -44,7 +46,8 @@ def launches(path):
         k = short(r[ki])
         tot[k] += float(r[vi].replace(",", ""))
         cnt[k] += 1
-    step = {k: tot[k] / cnt[k] for k in tot if k.startswith(("k_scan", "k_slide", "k_estimate"))}
+    pick = tuple(only.split(",")) if only else ("k_scan", "k_slide", "k_estimate")
+    step = {k: tot[k] / cnt[k] for k in tot if k.startswith(pick)}
     s = sum(step.values())
     print(f"{'avg ns':>12} {'count':>6} {'share of step':>14}  kernel")
     for k in sorted(tot, key=lambda k: -tot[k] / cnt[k]):
@@ -91,7 +94,7 @@ def traffic(rep, key_prefix):
 if __name__ == "__main__":
     cmd = sys.argv[1]
     if cmd == "launches":
-        launches(sys.argv[2])
+        launches(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
     elif cmd == "full":
         full(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "")
     elif cmd == "traffic":
