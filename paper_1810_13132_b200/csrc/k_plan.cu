@@ -229,9 +229,24 @@ __global__ void __launch_bounds__(kT) k_plan_pad(BuildArgs a) {
 // the entries, so the sums are unchanged; it cuts bank-conflict wavefronts
 // in k_estimate_plan.  Keys over the stage capacity are left alone (the
 // plan is refused anyway).
+// Lane j's entry of a round with `taken` real entries (lanes [0, taken)):
+// the padding lanes read the register word of the round's first entry (a
+// broadcast) and add into trash accumulators on the banks no real entry of
+// the round uses, so padding never adds a bank conflict.
+__device__ __forceinline__ uint32_t pad_round(uint32_t mine, uint32_t taken, uint32_t lane,
+                                              uint32_t kTrash) {
+  const bool real = lane < taken;
+  const uint32_t used = __reduce_or_sync(0xffffffffu, real ? 1u << ((mine >> 18) & 31u) : 0u);
+  const uint32_t off0 = __shfl_sync(0xffffffffu, mine, 0) & 0xFFFFu;
+  if (real) return mine;
+  const uint32_t bank = __fns(~used, 0, (int)(lane - taken) + 1);  // (lane - taken)-th free bank
+  return (taken ? off0 : 0u) | ((kTrash + (bank & 31u)) << 18);
+}
+
 __global__ void __launch_bounds__(kT) k_plan_sched(BuildArgs a, const uint32_t *range_size) {
   __shared__ uint32_t E[kCap];        // the key's entries: per group the remaining list
   __shared__ uint32_t cnt[kW][64];    // per warp: table-bank [0, 32) and acc-bank [32, 64) use
+  extern __shared__ uint8_t sched_dyn[];  // per warp: u8 loads [32 rounds][32 banks], two sides
   const uint64_t key = blockIdx.x;
   const uint32_t total = range_size[key];
   if (total > (uint32_t)kCap) return;
@@ -255,6 +270,46 @@ __global__ void __launch_bounds__(kT) k_plan_sched(BuildArgs a, const uint32_t *
     rem += __popc(m);
     __syncwarp();
   }
+  if (R <= 32u) {
+    // Best fit: each entry, in list order, goes to the round whose bank
+    // maxima it raises least -- register side plus accumulator side, i.e. the
+    // shared-memory wavefronts it adds to k_estimate_plan -- ties to the
+    // emptiest round.  Lane r keeps round r's fill and maxima; the rounds'
+    // per-bank loads live in shared memory.  (A round's base wavefront is
+    // free: the maxima start at 1.)
+    uint32_t *LRw = reinterpret_cast<uint32_t *>(sched_dyn + (size_t)w * 2048u);
+    for (uint32_t i = lane; i < 512u; i += 32u) LRw[i] = 0u;
+    uint8_t *LR = sched_dyn + (size_t)w * 2048u, *LA = LR + 1024u;
+    __syncwarp();
+    uint32_t fill = 0, mr = 1, ma = 1;
+    for (uint32_t e = 0; e < rem; ++e) {
+      const uint32_t v = L[e];
+      const uint32_t tb = (v >> 2) & 31u, ab = (v >> 18) & 31u;
+      uint32_t k = 0xFFFFFFFFu;
+      if (lane < R && fill < 32u) {
+        const uint32_t lr = LR[lane * 32u + tb] + 1u, la = LA[lane * 32u + ab] + 1u;
+        const uint32_t inc = (lr > mr ? lr - mr : 0u) + (la > ma ? la - ma : 0u);
+        k = (inc << 16) | (fill << 8) | lane;
+      }
+      const uint32_t bestr = __reduce_min_sync(0xffffffffu, k) & 0xFFu;
+      if (lane == bestr) {
+        out[32u * lane + fill] = v;
+        const uint32_t lr = ++LR[lane * 32u + tb], la = ++LA[lane * 32u + ab];
+        mr = max(mr, lr);
+        ma = max(ma, la);
+        ++fill;
+      }
+      __syncwarp();
+    }
+    for (uint32_t r = 0; r < R; ++r) {
+      const uint32_t taken = __shfl_sync(0xffffffffu, fill, r);
+      const uint32_t mine = lane < taken ? out[32u * r + lane] : 0u;
+      __syncwarp();
+      out[32u * r + lane] = pad_round(mine, taken, lane, kTrash);
+    }
+    return;
+  }
+  // more than 32 rounds (a few very full groups): round by round, greedy
   for (uint32_t r = 0; r < R; ++r) {
     const uint32_t target = min(32u, (rem + (R - r) - 1u) / (R - r));
     cnt[w][lane] = 0u;
@@ -292,19 +347,7 @@ __global__ void __launch_bounds__(kT) k_plan_sched(BuildArgs a, const uint32_t *
         __syncwarp();
       }
     }
-    // pad the round without adding a bank conflict: the padding reads the
-    // register word of the round's first entry (a broadcast) and adds into
-    // trash accumulators on the banks no real entry of the round uses
-    {
-      const bool real = lane < taken;
-      const uint32_t used = __reduce_or_sync(0xffffffffu, real ? 1u << ((mine >> 18) & 31u) : 0u);
-      const uint32_t off0 = __shfl_sync(0xffffffffu, mine, 0) & 0xFFFFu;
-      if (!real) {
-        const uint32_t bank = __fns(~used, 0, (int)(lane - taken) + 1);  // (lane - taken)-th free bank
-        mine = (taken ? off0 : 0u) | ((kTrash + (bank & 31u)) << 18);
-      }
-    }
-    out[32u * r + lane] = mine;
+    out[32u * r + lane] = pad_round(mine, taken, lane, kTrash);
     // drop the taken entries from the list
     uint32_t n2 = 0;
     for (uint32_t c = 0; c < rem; c += 32u) {
@@ -599,7 +642,9 @@ cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, 
   k_plan_bases<<<1, 1024, 0, s>>>(a, range_size_scratch, nkeys);
   k_plan_fill<<<grid ? grid : 1, 256, 0, s>>>(a);
   k_plan_pad<<<(uint32_t)nkeys, kT, 0, s>>>(a);
-  k_plan_sched<<<(uint32_t)nkeys, kT, 0, s>>>(a, range_size_scratch);
+  e = cudaFuncSetAttribute(k_plan_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, kW * 2048);
+  if (e != cudaSuccess) return e;
+  k_plan_sched<<<(uint32_t)nkeys, kT, kW * 2048, s>>>(a, range_size_scratch);
   return cudaGetLastError();
 }
 
