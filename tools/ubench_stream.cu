@@ -1,0 +1,166 @@
+// ubench_stream.cu -- what bounds the staged plan's block stream (round 2).
+// 148 persistent CTAs (one per SM), one producer lane issuing TMA bulk copies
+// of a table block (from a 4 MiB L2-resident array, the same block for every
+// CTA in a phase, as in k_estimate_plan) and of the CTA's own entry chunk
+// (from a 300 MB DRAM array, each CTA a contiguous region) into S stages;
+// 16 consumer warps wait for each stage, optionally touch it (one 4-byte
+// shared load per lane per 128 B: TOUCH=1), and release it.  L2 is flushed
+// before every timed launch.  Prints us per launch for the (T, E, S) given.
+// usage: ubench_stream T_bytes E_bytes stages phases [touch]
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) {                                                         \
+      fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_));     \
+      exit(1);                                                                       \
+    }                                                                                \
+  } while (0)
+
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mwait(uint64_t *bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                 : "=r"(done) : "r"(su32(bar)), "r"(parity) : "memory");
+}
+
+constexpr int kW = 16;
+
+__global__ void __launch_bounds__(kW * 32 + 32, 1)
+k_stream(const uint8_t *tab, const uint8_t *ent, uint32_t T, uint32_t E, uint32_t S,
+         uint32_t phases, int touch, unsigned long long *sink) {
+  extern __shared__ __align__(128) uint8_t raw[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(raw);
+  uint64_t *empty = full + 16;
+  uint8_t *buf = raw + 256;
+  const uint32_t stage = ((T + E) + 127u) & ~127u;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) {
+    for (uint32_t b = 0; b < S; ++b) {
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(su32(&full[b])));
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(su32(&empty[b])), "r"(kW));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint8_t *my_ent = ent + (uint64_t)blockIdx.x * phases * E;
+  if (w == kW) {
+    if (lane == 0) {
+      for (uint32_t ph = 0; ph < phases; ++ph) {
+        const uint32_t b = ph % S;
+        if (ph >= S) mwait(&empty[b], ((ph / S) + 1u) & 1u);
+        const uint32_t fb = su32(&full[b]);
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fb), "r"(T + E) : "memory");
+        uint8_t *dst = buf + (size_t)b * stage;
+        if (T)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(su32(dst)), "l"(tab + (uint64_t)(ph % 64) * T), "r"(T), "r"(fb) : "memory");
+        if (E)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(su32(dst + T)), "l"(my_ent + (uint64_t)ph * E), "r"(E), "r"(fb) : "memory");
+      }
+    }
+    return;
+  }
+  uint32_t acc = 0;
+  for (uint32_t ph = 0; ph < phases; ++ph) {
+    const uint32_t b = ph % S;
+    mwait(&full[b], (ph / S) & 1u);
+    if (touch) {
+      const uint32_t *p = reinterpret_cast<const uint32_t *>(buf + (size_t)b * stage);
+      for (uint32_t i = w * 32 + lane; i < (T + E) / 128u; i += kW * 32) acc += p[i * 32];
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(su32(&empty[b])) : "memory");
+  }
+  if (acc == 0x12345678u) atomicAdd(sink, 1ull);
+}
+
+// plain streaming read of `bytes` with 16-byte loads, UNROLL in flight per thread
+__global__ void __launch_bounds__(1024) k_ldg(const uint4 *p, uint64_t n16, unsigned long long *sink) {
+  uint32_t acc = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(p + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += v[u].x ^ v[u].w;
+  }
+  for (; i < n16; i += stride) acc += __ldcs(p + i).y;
+  if (acc == 0x12345678u) atomicAdd(sink, 1ull);
+}
+
+int main(int argc, char **argv) {
+  if (argc > 1 && argv[1][0] == 'L') {  // L <bytes>: the LDG read rate
+    const uint64_t bytes = strtoull(argv[2], nullptr, 10);
+    uint8_t *src, *flush;
+    unsigned long long *sink;
+    CK(cudaMalloc(&src, bytes));
+    CK(cudaMalloc(&flush, 512ull << 20));
+    CK(cudaMalloc(&sink, 8));
+    CK(cudaMemset(src, 3, bytes));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    float sum = 0;
+    for (int r = 0; r < 12; ++r) {
+      CK(cudaMemsetAsync(flush, r, 512ull << 20));
+      CK(cudaEventRecord(a));
+      k_ldg<<<148 * 2, 1024>>>(reinterpret_cast<const uint4 *>(src), bytes / 16, sink);
+      CK(cudaEventRecord(b));
+      CK(cudaEventSynchronize(b));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      if (r >= 2) sum += ms;
+    }
+    printf("LDG read %llu B: %.1f us, %.2f TB/s\n", (unsigned long long)bytes, 1e3 * sum / 10,
+           bytes / (sum / 10 * 1e-3) / 1e12);
+    return 0;
+  }
+  const uint32_t T = atoi(argv[1]), E = atoi(argv[2]), S = atoi(argv[3]), phases = atoi(argv[4]);
+  const int touch = argc > 5 ? atoi(argv[5]) : 0;
+  const int ctas = 148;
+  uint8_t *tab, *ent, *flush;
+  unsigned long long *sink;
+  CK(cudaMalloc(&tab, 64ull * (T ? T : 1)));
+  CK(cudaMalloc(&ent, (uint64_t)ctas * phases * (E ? E : 1)));
+  CK(cudaMalloc(&flush, 512ull << 20));
+  CK(cudaMalloc(&sink, 8));
+  CK(cudaMemset(tab, 1, 64ull * (T ? T : 1)));
+  CK(cudaMemset(ent, 2, (uint64_t)ctas * phases * (E ? E : 1)));
+  const uint32_t stage = ((T + E) + 127u) & ~127u;
+  const size_t smem = 256 + (size_t)S * stage;
+  CK(cudaFuncSetAttribute(k_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  float best = 1e30f, sum = 0;
+  const int reps = 10;
+  for (int r = 0; r < reps + 2; ++r) {
+    CK(cudaMemsetAsync(flush, r, 512ull << 20));
+    CK(cudaEventRecord(a));
+    k_stream<<<ctas, kW * 32 + 32, smem>>>(tab, ent, T, E, S, phases, touch, sink);
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    if (r >= 2) {
+      sum += ms;
+      if (ms < best) best = ms;
+    }
+  }
+  CK(cudaGetLastError());
+  const double bytes = (double)ctas * phases * (T + E);
+  printf("T=%u E=%u S=%u phases=%u touch=%d smem=%zu: %.1f us (best %.1f), %.2f TB/s into SMs, entries %.2f TB/s\n",
+         T, E, S, phases, touch, smem, 1e3 * sum / reps, 1e3 * best, bytes / (sum / reps * 1e-3) / 1e12,
+         (double)ctas * phases * E / (sum / reps * 1e-3) / 1e12);
+  return 0;
+}
