@@ -23,10 +23,15 @@ def main():
     ap.add_argument("--scan-mode", type=int, default=0)
     ap.add_argument("--estimate", default="staged")
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--config", default="caida", choices=["caida", "10G"])
+    ap.add_argument("--order", default="scan-first", choices=["scan-first", "estimate-first"],
+                    help="scan-first: bench.py's schedule (the estimate is enqueued after the "
+                         "scan, beside the slide); estimate-first: round 1's")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
-    tr = synth.CONFIGS["caida"]
-    pool = VBDR(128, 5, 1 << 22, scan_mode=args.scan_mode, device=dev)
+    tr = synth.CONFIGS[args.config]
+    m, k, z = (128, 5, 1 << 22) if args.config == "caida" else (256, 10, 1 << 26)
+    pool = VBDR(m, k, z, scan_mode=args.scan_mode, device=dev)
     gen = synth.DeviceTrace(tr, dev)
     inputs = []
     for t in range(8):
@@ -52,14 +57,18 @@ def main():
         flush.fill_(i & 0xFF)
         ev = {n: torch.cuda.Event(enable_timing=True) for n in names}
         ev["step0"].record(main_s)
+        if args.order == "scan-first":
+            pool.scan_slice(inputs[i % 8])
+            ev["scan_end"].record(main_s)
         closed = torch.cuda.Event()
         closed.record(main_s)
         side.wait_event(closed)
         ev["est_start"].record(side)
         est(side)
         ev["est_end"].record(side)
-        pool.scan_slice(inputs[i % 8])
-        ev["scan_end"].record(main_s)
+        if args.order != "scan-first":
+            pool.scan_slice(inputs[i % 8])
+            ev["scan_end"].record(main_s)
         pool.slide()
         ev["slide_end"].record(main_s)
         main_s.wait_event(ev["est_end"])
@@ -70,7 +79,7 @@ def main():
     for ev in rec[5:]:
         for n in names[1:]:
             t[n].append(ev["step0"].elapsed_time(ev[n]) * 1e3)
-    print(f"scan mode {args.scan_mode or 'default'}, {args.estimate} estimate, mean over "
+    print(f"{args.config}, {args.order}, scan mode {args.scan_mode or 'default'}, {args.estimate} estimate, mean over "
           f"{args.steps} pipelined steps (us from the step's start):")
     for n in names[1:]:
         print(f"  {n:10s} {np.mean(t[n]):8.1f}  (min {np.min(t[n]):.1f}, max {np.max(t[n]):.1f})")
