@@ -4,7 +4,8 @@
 usage: result_table.py <bench line .json> [...]
 
 One markdown row per line: config, layout, N, scan rate and its fraction of the
-L2 request ceiling the bench reports, slide time and HBM fraction, merge and
+ceiling the bench reports (layout F: the scan's memory path on the workload's
+update stream; P, S: the SM-to-L2 random-request rate), slide time and HBM fraction, merge and
 estimate times, gathers/s, the step (pipelined / serial / gather), e2e, the
 oracle's rate when the line carries it.  Parity is the GPU test log's verdict
 for that config (passed in with --parity, default "green")."""
@@ -21,11 +22,12 @@ def row(d: dict, parity: str) -> str:
     step = d["ms_per_step"]
     serial = d.get("ms_per_step_serial")
     gather = d.get("ms_per_step_gather")
-    return ("| {w} | {lay} | {n} | {scan:,.0f} | {sfrac:.2f} | {slms:.4f} | {slgb:,.0f} ({slf:.0%}) | "
+    sb = {"scan_memory_path": "memory path", "l2_requests": "L2 requests"}.get(sc.get("bound"), "?")
+    return ("| {w} | {lay} | {n} | {scan:,.0f} | {sfrac:.2f} ({sb}) | {slms:.4f} | {slgb:,.0f} ({slf:.0%}) | "
             "{merge} | {est:.4f} ({path}) | {gps:.1f} G | {step:.4f} / {ser} / {gat} | {val:,.0f} | "
             "{e2e} | {cpu} | {par} |").format(
         w=c["workload"], lay=c["layout"], n=d["n_gpus"],
-        scan=d["scan_mpairs_s"], sfrac=sc["frac"], slms=d["slide_ms"], slgb=sl["achieved"],
+        scan=d["scan_mpairs_s"], sfrac=sc["frac"], sb=sb, slms=d["slide_ms"], slgb=sl["achieved"],
         slf=sl["frac"], merge="—" if d["n_gpus"] == 1 else f"{d['merge_ms']:.4f}",
         est=d["estimate_ms"], path=c.get("estimate_path", "?"),
         gps=es["gathers_per_s"] / 1e9, step=step,
@@ -34,7 +36,7 @@ def row(d: dict, parity: str) -> str:
         cpu=f"{cpu['value']:.2f}" if cpu.get("value") else "—", par=parity)
 
 
-HEADER = ("| config | layout | N | scan Mpairs/s | scan / L2 request ceiling | slide ms | "
+HEADER = ("| config | layout | N | scan Mpairs/s | scan / its ceiling | slide ms | "
           "slide GB/s (of 6549.8) | merge ms | estimate ms (path) | gathers/s | "
           "step ms (headline / serial / gather estimate) | value Mpairs/s | e2e Mpairs/s | "
           "oracle Mpairs/s (1 core) | parity |\n"
