@@ -315,14 +315,17 @@ vbdr_status vbdr_select_above(vbdr_t *h, const double *d_est, uint64_t n, double
  *    n_phys >= 128.  Plan: 4 B per (host, i) plus the bucket table
  *    (n_phys * P / 128 * 4 B).  One estimate per plan at a time (stream-ordered).
  *  - VBDR_PLAN_STAGED (k_plan.cu): the register array streamed through shared
- *    memory in 64 KB blocks by TMA, (host, i) entries grouped by block and
- *    warp in bank-scheduled rounds; n_phys in [64, 2^22], n_hosts <= 7 * 512
- *    * SMs.
+ *    memory in blocks of up to 64 KB by TMA, (host, i) entries grouped by
+ *    block and warp in bank-scheduled rounds (4 B per (host, i)); n_phys in
+ *    [64, 2^22]; the hosts' accumulators (8 B per host per CTA) share the
+ *    SM's shared memory with the stages, so larger host lists get smaller
+ *    blocks (caida's 500 k hosts: 64 KB; 1.2 M: 16 KB).
  *  - VBDR_PLAN_PASSID (k_estimate.cu): for pools whose gather estimate runs
  *    in 2..4 passes (est_pass_log2), 64 <= g <= 2048: the pass of every
  *    (host, i) in 2 bits, so each pass hashes and gathers only its registers.
- * VBDR_PLAN_AUTO takes the first that fits in the order SORTED, STAGED,
- * PASSID; otherwise VBDR_ERANGE. */
+ * VBDR_PLAN_AUTO takes STAGED when it fits and n_hosts * m >= n_phys (the
+ * gathers outnumber the registers every SM streams), else the first that
+ * fits in the order SORTED, STAGED, PASSID; otherwise VBDR_ERANGE. */
 typedef enum {
     VBDR_PLAN_AUTO = 0,
     VBDR_PLAN_STAGED = 1,

@@ -813,6 +813,11 @@ bool passplan_geom(const vbdr *h, uint64_t n_hosts, PassPlanGeom *g) {
 // (pass ids), or -1.  VBDR_PLAN_AUTO takes the first that fits in that order.
 int choose_plan(const vbdr *h, uint64_t n_hosts, uint32_t want, PlanGeom *g, PassPlanGeom *pg,
                 SpGeom *sg) {
+  // AUTO: the staged plan when its gathers outnumber the registers it streams
+  // through every SM (caida: 16 per register, 82 vs ~100 us for the sorted
+  // plan; profiles/r02_sorted_plan.txt), else the sorted plan, else pass ids
+  if (want == VBDR_PLAN_AUTO && n_hosts * h->cfg.m >= h->p.n_phys && plan_geom(h, n_hosts, g))
+    return 0;
   if ((want == VBDR_PLAN_AUTO || want == VBDR_PLAN_SORTED) && sp_geom(h, n_hosts, sg)) return 2;
   if ((want == VBDR_PLAN_AUTO || want == VBDR_PLAN_STAGED) && plan_geom(h, n_hosts, g)) return 0;
   if ((want == VBDR_PLAN_AUTO || want == VBDR_PLAN_PASSID) && passplan_geom(h, n_hosts, pg)) return 1;

@@ -359,8 +359,8 @@ class VBDR:
     def plan(self, hosts, kind: str = "auto", stream=None):
         """``vbdr_plan_bytes_kind`` + ``vbdr_plan_build_kind``: preprocess a
         fixed host list (device u32/int32 tensor) for repeated estimates --
-        kind "sorted", "staged", "passid" or "auto" (the first that fits, in
-        that order; include/vbdr.h).  Returns an :class:`EstimatePlan`; raises
+        kind "sorted", "staged", "passid" or "auto" (staged for dense host
+        lists, else the first that fits; include/vbdr.h vbdr_plan_kind).  Returns an :class:`EstimatePlan`; raises
         ValueError when the pool or host count has no plan of that kind (use
         :meth:`estimate`)."""
         import torch
