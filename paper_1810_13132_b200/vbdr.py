@@ -382,6 +382,7 @@ class VBDR:
     def estimate_plan(self, plan: "EstimatePlan", out=None, stream=None):
         """``vbdr_estimate_plan``: estimates for the plan's hosts (float64)."""
         import torch
+        plan.check_live()
         if out is None:
             out = torch.empty(plan.n_hosts, dtype=torch.float64, device=self.device)
         self._check(lib().vbdr_estimate_plan(self._h, C.c_void_p(plan.buf.data_ptr()),
@@ -391,6 +392,7 @@ class VBDR:
 
     def estimate_plan_host(self, plan: "EstimatePlan", d_out_stage, h_out, stream=None):
         """``vbdr_estimate_plan_host``: estimates copied into a (pinned) CPU tensor."""
+        plan.check_live()
         self._check(lib().vbdr_estimate_plan_host(self._h, C.c_void_p(plan.buf.data_ptr()),
                                                   C.c_void_p(d_out_stage.data_ptr()),
                                                   C.c_void_p(h_out.data_ptr()),
@@ -398,6 +400,7 @@ class VBDR:
 
     def host_sums_plan(self, plan: "EstimatePlan", stream=None):
         import torch
+        plan.check_live()
         S = torch.empty(plan.n_hosts, dtype=torch.int64, device=self.device)
         V = torch.empty(plan.n_hosts, dtype=torch.int32, device=self.device)
         self._check(lib().vbdr_host_sums_plan(self._h, C.c_void_p(plan.buf.data_ptr()),
@@ -406,6 +409,7 @@ class VBDR:
         return S, V
 
     def plan_check(self, plan: "EstimatePlan", stream=None):
+        plan.check_live()
         self._check(lib().vbdr_plan_check(self._h, C.c_void_p(plan.buf.data_ptr()),
                                           _stream_ptr(stream)), "vbdr_plan_check")
 
@@ -487,6 +491,10 @@ class EstimatePlan:
     @property
     def nbytes(self) -> int:
         return self.buf.numel()
+
+    def check_live(self):
+        if self.buf is None:
+            raise ValueError("this estimate plan was released")
 
     def release(self):
         if self.buf is not None and getattr(self.pool, "_h", None):

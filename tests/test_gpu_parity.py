@@ -609,6 +609,42 @@ def test_abi_errors():
     assert pool.estimate(torch.zeros(0, dtype=torch.int32, device=DEV)).numel() == 0
 
 
+def test_plan_abi_errors():
+    """Plan calls fail loudly and launch nothing: a plan of another handle, a
+    released plan, a buffer too small or misaligned, an unknown kind."""
+    import ctypes as C
+    from paper_1810_13132_b200.vbdr import lib
+    a = VBDR(32, 4, 1 << 12, device=DEV)
+    b = VBDR(32, 4, 1 << 12, device=DEV)
+    hosts = dev_u32(synth.CONFIGS["tiny"].host_ids())
+    plan = a.plan(hosts, kind="staged")
+    before = b.info()["launches"]
+    with pytest.raises(RuntimeError, match="EINVAL"):
+        b.estimate_plan(plan)  # built by handle a
+    assert b.info()["launches"] == before
+    p2 = a.plan(hosts, kind="sorted")
+    ptr = p2.buf.data_ptr()
+    p2.release()
+    with pytest.raises(ValueError, match="released"):
+        a.estimate_plan(p2)
+    out = torch.empty(hosts.numel(), dtype=torch.float64, device=DEV)
+    assert lib().vbdr_estimate_plan(a._h, C.c_void_p(ptr), C.c_void_p(out.data_ptr()), None) == -1
+    need = C.c_uint64()
+    assert lib().vbdr_plan_bytes_kind(a._h, hosts.numel(), 1, C.byref(need)) == 0
+    buf = torch.empty(need.value + 512, dtype=torch.uint8, device=DEV)
+    rc = lib().vbdr_plan_build_kind(a._h, C.c_void_p(hosts.data_ptr()), hosts.numel(), 1,
+                                    C.c_void_p(buf.data_ptr()), need.value - 256, None)
+    assert rc == -4  # ENOMEM: buffer too small
+    rc = lib().vbdr_plan_build_kind(a._h, C.c_void_p(hosts.data_ptr()), hosts.numel(), 1,
+                                    C.c_void_p(buf.data_ptr() + 16), need.value, None)
+    assert rc == -1  # EINVAL: not 256-byte aligned
+    assert lib().vbdr_plan_bytes_kind(a._h, hosts.numel(), 9, C.byref(need)) == -1
+    with pytest.raises(KeyError):
+        a.plan(hosts, kind="nope")
+    # the plan of handle a still works
+    assert np.array_equal(a.estimate_plan(plan).cpu().numpy(), a.estimate(hosts).cpu().numpy())
+
+
 @pytest.mark.parametrize("n_ranks", [2, 4, 8])
 def test_loopback_fused_peer_merge_slide(n_ranks):
     """vbdr_slide_peers with virtual peers on one GPU: rank r's kernel reads
