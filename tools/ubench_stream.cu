@@ -35,11 +35,16 @@ constexpr int kW = 16;
 __global__ void __launch_bounds__(kW * 32 + 32, 1)
 k_stream(const uint8_t *tab, const uint8_t *ent, uint32_t T, uint32_t E, uint32_t S,
          uint32_t phases, int touch, unsigned long long *sink) {
+  // touch = 2: the entries are NOT staged; the consumer warps read their
+  // share of each phase's entry chunk straight from global memory (16-byte
+  // loads), the producer prefetches the next chunk into L2
+  const bool ldg = touch == 2;
+  const uint32_t Es = ldg ? 0u : E;
   extern __shared__ __align__(128) uint8_t raw[];
   uint64_t *full = reinterpret_cast<uint64_t *>(raw);
   uint64_t *empty = full + 16;
   uint8_t *buf = raw + 256;
-  const uint32_t stage = ((T + E) + 127u) & ~127u;
+  const uint32_t stage = ((T + (touch == 2 ? 0u : E)) + 127u) & ~127u;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) {
     for (uint32_t b = 0; b < S; ++b) {
@@ -56,14 +61,17 @@ k_stream(const uint8_t *tab, const uint8_t *ent, uint32_t T, uint32_t E, uint32_
         const uint32_t b = ph % S;
         if (ph >= S) mwait(&empty[b], ((ph / S) + 1u) & 1u);
         const uint32_t fb = su32(&full[b]);
-        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fb), "r"(T + E) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fb), "r"(T + Es) : "memory");
         uint8_t *dst = buf + (size_t)b * stage;
         if (T)
           asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                        ::"r"(su32(dst)), "l"(tab + (uint64_t)(ph % 64) * T), "r"(T), "r"(fb) : "memory");
-        if (E)
+        if (Es)
           asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                        ::"r"(su32(dst + T)), "l"(my_ent + (uint64_t)ph * E), "r"(E), "r"(fb) : "memory");
+        if (ldg && ph + 1 < phases)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(my_ent + (uint64_t)(ph + 1) * E),
+                       "r"(E) : "memory");
       }
     }
     return;
@@ -72,7 +80,15 @@ k_stream(const uint8_t *tab, const uint8_t *ent, uint32_t T, uint32_t E, uint32_
   for (uint32_t ph = 0; ph < phases; ++ph) {
     const uint32_t b = ph % S;
     mwait(&full[b], (ph / S) & 1u);
-    if (touch) {
+    if (ldg) {
+      const uint4 *q = reinterpret_cast<const uint4 *>(my_ent + (uint64_t)ph * E);
+      const uint32_t n16 = E / 16u;
+#pragma unroll 4
+      for (uint32_t i = w * 32 + lane; i < n16; i += kW * 32) {
+        const uint4 v = __ldcs(q + i);
+        acc += v.x ^ v.w;
+      }
+    } else if (touch) {
       const uint32_t *p = reinterpret_cast<const uint32_t *>(buf + (size_t)b * stage);
       for (uint32_t i = w * 32 + lane; i < (T + E) / 128u; i += kW * 32) acc += p[i * 32];
     }
@@ -136,7 +152,7 @@ int main(int argc, char **argv) {
   CK(cudaMalloc(&sink, 8));
   CK(cudaMemset(tab, 1, 64ull * (T ? T : 1)));
   CK(cudaMemset(ent, 2, (uint64_t)ctas * phases * (E ? E : 1)));
-  const uint32_t stage = ((T + E) + 127u) & ~127u;
+  const uint32_t stage = ((T + (touch == 2 ? 0u : E)) + 127u) & ~127u;
   const size_t smem = 256 + (size_t)S * stage;
   CK(cudaFuncSetAttribute(k_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t a, b;
