@@ -93,7 +93,7 @@ def main():
         sr = torch.zeros(z, dtype=torch.int32, device=dev)
         s = torch.cuda.current_stream(dev)
         out = {}
-        for mode, key in ((0, "check_then_atomic"), (1, "atomic_only")):
+        for mode, key in ((0, "check_then_atomic"), (1, "atomic_only"), (2, "u8_check_then_cas")):
             ts = []
             for r in range(args.reps + 2):
                 sr.zero_()

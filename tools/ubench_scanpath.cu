@@ -5,7 +5,8 @@
 // record like the IP pairs; the kernel streams them with the scan's 16-byte
 // loads and grid, and does exactly the scan's global traffic per record --
 // mode 0: the L2 check load, then atomicMax when the stored value is smaller
-// (k_scan mode 2 without hashing); mode 1: atomicMax on every record.  No
+// (k_scan mode 2 without hashing); mode 1: atomicMax on every record; mode 2:
+// a u8 per register (z bytes) -- check the byte, then atomicCAS on its word.  No
 // hashing, no shared-memory cache: what is left is the cost of the memory
 // path, so k_scan's rate over this one is its fraction of the path's bound.
 // Built as a shared library (extern "C"), called through ctypes.
@@ -17,6 +18,17 @@ namespace {
 constexpr int kThreads = 256;
 
 __device__ __forceinline__ void rec(uint32_t j, uint32_t val, uint32_t *sr, int mode) {
+  if (mode == 2) {  // u8 per register (the paper's nowLBP1): check the byte, CAS the word
+    uint32_t *w = sr + (j >> 2);
+    const uint32_t sh = (j & 3u) * 8u, rho = val & 31u;
+    uint32_t cur = __ldcg(w);
+    while (((cur >> sh) & 0xFFu) < rho) {
+      const uint32_t prev = atomicCAS(w, cur, (cur & ~(0xFFu << sh)) | (rho << sh));
+      if (prev == cur) break;
+      cur = prev;
+    }
+    return;
+  }
   if (mode == 0 && __ldcg(sr + j) >= val) return;
   atomicMax(sr + j, val);
 }
