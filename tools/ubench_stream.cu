@@ -98,6 +98,72 @@ k_stream(const uint8_t *tab, const uint8_t *ent, uint32_t T, uint32_t E, uint32_
   if (acc == 0x12345678u) atomicAdd(sink, 1ull);
 }
 
+
+// Decoupled rings (round 2): table blocks in ST stages, entry chunks in SE
+// stages, each with its own full/empty barriers, so the DRAM-bound entry
+// stream can run further ahead than the L2-bound table stream.
+__global__ void __launch_bounds__(kW * 32 + 32, 1)
+k_stream2(const uint8_t *tab, const uint8_t *ent, uint32_t T, uint32_t E, uint32_t ST,
+          uint32_t SE, uint32_t phases, unsigned long long *sink) {
+  extern __shared__ __align__(128) uint8_t raw[];
+  uint64_t *tfull = reinterpret_cast<uint64_t *>(raw), *tempty = tfull + 8;
+  uint64_t *efull = tfull + 16, *eempty = tfull + 24;
+  uint8_t *tbuf = raw + 256;
+  const uint32_t estage = (E + 127u) & ~127u;
+  uint8_t *ebuf = tbuf + (size_t)ST * T;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) {
+    for (uint32_t b = 0; b < ST; ++b) {
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(su32(&tfull[b])));
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(su32(&tempty[b])), "r"(kW));
+    }
+    for (uint32_t b = 0; b < SE; ++b) {
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(su32(&efull[b])));
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(su32(&eempty[b])), "r"(kW));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint8_t *my_ent = ent + (uint64_t)blockIdx.x * phases * E;
+  if (w == kW) {
+    if (lane == 0) {
+      // entries run up to SE phases ahead, tables up to ST
+      uint32_t te = 0, tt = 0;
+      while (tt < phases) {
+        while (te < phases && te < tt + SE) {
+          const uint32_t b = te % SE;
+          if (te >= SE) mwait(&eempty[b], ((te / SE) + 1u) & 1u);
+          const uint32_t fb = su32(&efull[b]);
+          asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fb), "r"(E) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(su32(ebuf + (size_t)b * estage)), "l"(my_ent + (uint64_t)te * E), "r"(E), "r"(fb) : "memory");
+          ++te;
+        }
+        const uint32_t b = tt % ST;
+        if (tt >= ST) mwait(&tempty[b], ((tt / ST) + 1u) & 1u);
+        const uint32_t fb = su32(&tfull[b]);
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fb), "r"(T) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(su32(tbuf + (size_t)b * T)), "l"(tab + (uint64_t)(tt % 64) * T), "r"(T), "r"(fb) : "memory");
+        ++tt;
+      }
+    }
+    return;
+  }
+  uint32_t acc = 0;
+  for (uint32_t ph = 0; ph < phases; ++ph) {
+    mwait(&tfull[ph % ST], (ph / ST) & 1u);
+    mwait(&efull[ph % SE], (ph / SE) & 1u);
+    acc += tbuf[(size_t)(ph % ST) * T + lane] + ebuf[(size_t)(ph % SE) * estage + lane];
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(su32(&tempty[ph % ST])) : "memory");
+      asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(su32(&eempty[ph % SE])) : "memory");
+    }
+  }
+  if (acc == 0x12345678u) atomicAdd(sink, 1ull);
+}
+
 // plain streaming read of `bytes` with 16-byte loads, UNROLL in flight per thread
 __global__ void __launch_bounds__(1024) k_ldg(const uint4 *p, uint64_t n16, unsigned long long *sink) {
   uint32_t acc = 0;
@@ -115,6 +181,38 @@ __global__ void __launch_bounds__(1024) k_ldg(const uint4 *p, uint64_t n16, unsi
 }
 
 int main(int argc, char **argv) {
+  if (argc > 1 && argv[1][0] == 'R') {  // R T E ST SE phases: decoupled rings
+    const uint32_t T = atoi(argv[2]), E = atoi(argv[3]), ST = atoi(argv[4]), SE = atoi(argv[5]),
+                   phases = atoi(argv[6]);
+    uint8_t *tab, *ent, *flush;
+    unsigned long long *sink;
+    CK(cudaMalloc(&tab, 64ull * T));
+    CK(cudaMalloc(&ent, 148ull * phases * E));
+    CK(cudaMalloc(&flush, 512ull << 20));
+    CK(cudaMalloc(&sink, 8));
+    CK(cudaMemset(tab, 1, 64ull * T));
+    CK(cudaMemset(ent, 2, 148ull * phases * E));
+    const size_t smem = 256 + (size_t)ST * T + (size_t)SE * ((E + 127u) & ~127u);
+    CK(cudaFuncSetAttribute(k_stream2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    float sum = 0;
+    for (int r = 0; r < 12; ++r) {
+      CK(cudaMemsetAsync(flush, r, 512ull << 20));
+      CK(cudaEventRecord(a));
+      k_stream2<<<148, kW * 32 + 32, smem>>>(tab, ent, T, E, ST, SE, phases, sink);
+      CK(cudaEventRecord(b));
+      CK(cudaEventSynchronize(b));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      if (r >= 2) sum += ms;
+    }
+    CK(cudaGetLastError());
+    printf("rings T=%u x %u, E=%u x %u, phases=%u, smem=%zu: %.1f us\n", T, ST, E, SE, phases, smem,
+           1e3 * sum / 10);
+    return 0;
+  }
   if (argc > 1 && argv[1][0] == 'L') {  // L <bytes>: the LDG read rate
     const uint64_t bytes = strtoull(argv[2], nullptr, 10);
     uint8_t *src, *flush;
