@@ -39,6 +39,9 @@ using vbdr_launch::PlanLayout;
 
 namespace {
 
+#ifndef VBDR_PLAN_ILP
+#define VBDR_PLAN_ILP 4  // rounds whose loads are issued before their atomics
+#endif
 #ifndef VBDR_PLAN_PREFETCH
 #define VBDR_PLAN_PREFETCH 1  // phases ahead (0 = off; profiles/r01_plan_variants.txt)
 #endif
@@ -441,7 +444,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
                 unsigned long long *__restrict__ outS, uint32_t *__restrict__ outV,
                 unsigned long long *__restrict__ err) {
   constexpr uint32_t BLOCK = 1u << BLOCK_LOG2;
-  constexpr int ILP = 4;
+  constexpr int ILP = VBDR_PLAN_ILP;
   pdl_wait();
   extern __shared__ __align__(128) uint8_t raw[];
   PlanSmem<BLOCK_LOG2> &sm = *reinterpret_cast<PlanSmem<BLOCK_LOG2> *>(raw);
