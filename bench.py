@@ -713,10 +713,12 @@ def run_vbdr(args):
     g_rate = gathers / (kern["estimate"] * 1e-3) / 1e9
     scan_rate = n_local / (kern["scan"] * 1e-3) / 1e9
     req_peak = ceil["ldg_gather_1B_Gps"]["4MiB"]
-    path_peak = ceil.get("scan_path_Gpairs_s", {}).get(args.config) if args.layout == "fast" else None
+    path_key = {"fast": "scan_path_Gpairs_s", "packed": "scan_path_packed_Gpairs_s"}.get(args.layout)
+    path_peak = ceil.get(path_key, {}).get(args.config) if path_key else None
     if path_peak:
         # the scan's own memory path on this workload's update stream (check
-        # load + atomicMax per pair, no hashing, no shared-memory cache)
+        # load + atomicMax per pair -- layout P: + atomicAnd of the field --
+        # no hashing, no shared-memory cache)
         scan_roof = {"bound": "scan_memory_path", "peak": path_peak,
                      "frac": round(scan_rate / path_peak, 4),
                      "peak_source": ceil.get("scan_path_source", "profiles/ceilings_b200.json")

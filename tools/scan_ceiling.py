@@ -27,6 +27,7 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 WL = {"caida": (128, 1 << 22), "10G": (256, 1 << 26), "bigwin": (256, 1 << 28)}
+K = {"caida": 5, "10G": 10, "bigwin": 60}
 A0, A1 = 0x5EED0001, 0x5EED0002
 M32 = 0xFFFFFFFF
 
@@ -49,7 +50,13 @@ def clz32(x):
     return n + (x == 0).to(n.dtype)
 
 
-def records(name: str, dev, T: int = 7):
+def packed_zb(k: int) -> int:
+    """Layout P's DR width: ceil(log2(k+1)), one more when 2^zb - 2 < k (vbdr.h zbits)."""
+    zb = max(1, k.bit_length())
+    return zb + 1 if (1 << zb) - 2 < k else zb
+
+
+def records(name: str, dev, T: int = 7, packed: bool = False):
     m, z = WL[name]
     b = m.bit_length() - 1
     L = 32 - b
@@ -64,11 +71,18 @@ def records(name: str, dev, T: int = 7):
     rho = torch.clamp(clz32(w) + 1, max=L)
     j = fmix32(aip ^ fmix32(vidx ^ A0)) & (z - 1)
     val = (T << 5) | rho
+    if packed:  # the DRV word of rank rho and the field's mask (plane-major, F fields per word)
+        zb = packed_zb(K[name])
+        F = 32 // zb
+        r = rho - 1
+        j = (r // F) * z + j
+        val = ((1 << zb) - 1) << (zb * (r % F))
     out = torch.stack([j, val], dim=1).to(torch.int64)
     out = torch.where(out >= 1 << 31, out - (1 << 32), out).to(torch.int32)
     if out.shape[0] % 2:
         out = out[:-1]
-    return out.contiguous(), z
+    W = -(-(32 - b) // (32 // packed_zb(K[name]))) if packed else 1
+    return out.contiguous(), z * W
 
 
 def main():
@@ -91,26 +105,33 @@ def main():
     for name in args.configs.split(","):
         rec, z = records(name, dev)
         sr = torch.zeros(z, dtype=torch.int32, device=dev)
+        prec, pz = records(name, dev, packed=True)
+        drv = torch.empty(pz, dtype=torch.int32, device=dev)
         s = torch.cuda.current_stream(dev)
         out = {}
-        for mode, key in ((0, "check_then_atomic"), (1, "atomic_only"), (2, "u8_check_then_cas")):
+        for mode, key in ((0, "check_then_atomic"), (1, "atomic_only"), (2, "u8_check_then_cas"),
+                          (3, "packed_check_then_and")):
             ts = []
+            arr, recs = (drv, prec) if mode == 3 else (sr, rec)
             for r in range(args.reps + 2):
-                sr.zero_()
+                if mode == 3:
+                    arr.fill_(-1)  # InitDR: every field saturated (all ones)
+                else:
+                    arr.zero_()
                 flush.fill_(r & 0xFF)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(s)
-                assert lib.sp_run(rec.data_ptr(), rec.shape[0], sr.data_ptr(), mode,
+                assert lib.sp_run(recs.data_ptr(), recs.shape[0], arr.data_ptr(), mode,
                                   ctypes.c_void_p(s.cuda_stream)) == 0
                 e1.record(s)
                 torch.cuda.synchronize()
                 if r >= 2:
                     ts.append(e0.elapsed_time(e1))
             ms = sum(ts) / len(ts)
-            out[key] = round(rec.shape[0] / (ms * 1e-3) / 1e9, 2)
+            out[key] = round(recs.shape[0] / (ms * 1e-3) / 1e9, 2)
             out[key + "_ms"] = round(ms, 5)
         res[name] = out
-        del rec, sr
+        del rec, sr, prec, drv
         torch.cuda.empty_cache()
     print(json.dumps(res))
     if args.write:
@@ -118,6 +139,7 @@ def main():
         with open(path) as f:
             c = json.load(f)
         c["scan_path_Gpairs_s"] = {k: v["check_then_atomic"] for k, v in res.items()}
+        c["scan_path_packed_Gpairs_s"] = {k: v["packed_check_then_and"] for k, v in res.items()}
         c["scan_path_detail"] = res
         c["scan_path_source"] = ("tools/scan_ceiling.py + tools/ubench_scanpath.cu: the bench's "
                                  "slice hashed to (register, stamp) records, streamed through "

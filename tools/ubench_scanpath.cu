@@ -6,7 +6,8 @@
 // loads and grid, and does exactly the scan's global traffic per record --
 // mode 0: the L2 check load, then atomicMax when the stored value is smaller
 // (k_scan mode 2 without hashing); mode 1: atomicMax on every record; mode 2:
-// a u8 per register (z bytes) -- check the byte, then atomicCAS on its word.  No
+// a u8 per register (z bytes) -- check the byte, then atomicCAS on its word;
+// mode 3: layout P's SetDR -- check the field, then atomicAnd clearing it.  No
 // hashing, no shared-memory cache: what is left is the cost of the memory
 // path, so k_scan's rate over this one is its fraction of the path's bound.
 // Built as a shared library (extern "C"), called through ctypes.
@@ -27,6 +28,11 @@ __device__ __forceinline__ void rec(uint32_t j, uint32_t val, uint32_t *sr, int 
       if (prev == cur) break;
       cur = prev;
     }
+    return;
+  }
+  if (mode == 3) {  // layout P: val = the field mask of rank rho in word j (SetDR, Alg.9)
+    if ((__ldcg(sr + j) & val) == 0u) return;  // already cleared
+    atomicAnd(sr + j, ~val);
     return;
   }
   if (mode == 0 && __ldcg(sr + j) >= val) return;
