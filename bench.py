@@ -713,7 +713,8 @@ def run_vbdr(args):
     g_rate = gathers / (kern["estimate"] * 1e-3) / 1e9
     scan_rate = n_local / (kern["scan"] * 1e-3) / 1e9
     req_peak = ceil["ldg_gather_1B_Gps"]["4MiB"]
-    path_key = {"fast": "scan_path_Gpairs_s", "packed": "scan_path_packed_Gpairs_s"}.get(args.layout)
+    path_key = {"fast": "scan_path_Gpairs_s", "packed": "scan_path_packed_Gpairs_s",
+                "stamps": "scan_path_stamps_Gpairs_s"}.get(args.layout)
     path_peak = ceil.get(path_key, {}).get(args.config) if path_key else None
     if path_peak:
         # the scan's own memory path on this workload's update stream (check

@@ -56,7 +56,7 @@ def packed_zb(k: int) -> int:
     return zb + 1 if (1 << zb) - 2 < k else zb
 
 
-def records(name: str, dev, T: int = 7, packed: bool = False):
+def records(name: str, dev, T: int = 7, packed: bool = False, stamps: bool = False):
     m, z = WL[name]
     b = m.bit_length() - 1
     L = 32 - b
@@ -71,6 +71,9 @@ def records(name: str, dev, T: int = 7, packed: bool = False):
     rho = torch.clamp(clz32(w) + 1, max=L)
     j = fmix32(aip ^ fmix32(vidx ^ A0)) & (z - 1)
     val = (T << 5) | rho
+    if stamps:  # layout S: the stamp of (rank rho, register j), L planes of z words; value T
+        j = (rho - 1) * z + j
+        val = torch.full_like(j, T)
     if packed:  # the DRV word of rank rho and the field's mask (plane-major, F fields per word)
         zb = packed_zb(K[name])
         F = 32 // zb
@@ -81,7 +84,7 @@ def records(name: str, dev, T: int = 7, packed: bool = False):
     out = torch.where(out >= 1 << 31, out - (1 << 32), out).to(torch.int32)
     if out.shape[0] % 2:
         out = out[:-1]
-    W = -(-(32 - b) // (32 // packed_zb(K[name]))) if packed else 1
+    W = -(-(32 - b) // (32 // packed_zb(K[name]))) if packed else (L if stamps else 1)
     return out.contiguous(), z * W
 
 
@@ -107,12 +110,15 @@ def main():
         sr = torch.zeros(z, dtype=torch.int32, device=dev)
         prec, pz = records(name, dev, packed=True)
         drv = torch.empty(pz, dtype=torch.int32, device=dev)
+        srec, sz = records(name, dev, stamps=True) if name != "bigwin" else (None, 0)
+        st = torch.zeros(sz, dtype=torch.int32, device=dev) if sz else None
         s = torch.cuda.current_stream(dev)
         out = {}
-        for mode, key in ((0, "check_then_atomic"), (1, "atomic_only"), (2, "u8_check_then_cas"),
-                          (3, "packed_check_then_and")):
+        modes = [(0, "check_then_atomic"), (1, "atomic_only"), (2, "u8_check_then_cas"),
+                 (3, "packed_check_then_and")] + ([(4, "stamps_check_then_atomic")] if sz else [])
+        for mode, key in modes:
             ts = []
-            arr, recs = (drv, prec) if mode == 3 else (sr, rec)
+            arr, recs = {3: (drv, prec), 4: (st, srec)}.get(mode, (sr, rec))
             for r in range(args.reps + 2):
                 if mode == 3:
                     arr.fill_(-1)  # InitDR: every field saturated (all ones)
@@ -121,7 +127,7 @@ def main():
                 flush.fill_(r & 0xFF)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(s)
-                assert lib.sp_run(recs.data_ptr(), recs.shape[0], arr.data_ptr(), mode,
+                assert lib.sp_run(recs.data_ptr(), recs.shape[0], arr.data_ptr(), 0 if mode == 4 else mode,
                                   ctypes.c_void_p(s.cuda_stream)) == 0
                 e1.record(s)
                 torch.cuda.synchronize()
@@ -131,7 +137,7 @@ def main():
             out[key] = round(recs.shape[0] / (ms * 1e-3) / 1e9, 2)
             out[key + "_ms"] = round(ms, 5)
         res[name] = out
-        del rec, sr, prec, drv
+        del rec, sr, prec, drv, srec, st
         torch.cuda.empty_cache()
     print(json.dumps(res))
     if args.write:
@@ -140,6 +146,8 @@ def main():
             c = json.load(f)
         c["scan_path_Gpairs_s"] = {k: v["check_then_atomic"] for k, v in res.items()}
         c["scan_path_packed_Gpairs_s"] = {k: v["packed_check_then_and"] for k, v in res.items()}
+        c["scan_path_stamps_Gpairs_s"] = {k: v["stamps_check_then_atomic"] for k, v in res.items()
+                                          if "stamps_check_then_atomic" in v}
         c["scan_path_detail"] = res
         c["scan_path_source"] = ("tools/scan_ceiling.py + tools/ubench_scanpath.cu: the bench's "
                                  "slice hashed to (register, stamp) records, streamed through "
