@@ -749,7 +749,14 @@ def run_vbdr(args):
                      "peak_source": hbm_src,
                      "note": "algorithmic bytes = SURVEY 8(d.4): 4 B host in + 8 B out + g x "
                              "1 B registers per host; traffic_impl = what the path streams "
-                             "by design (plan entries, 4 B per gather)"},
+                             "by design (plan entries, 4 B per gather)",
+                     # context: the staged plan's own stream alone (tools/ubench_stream.cu)
+                     **({"stream_floor_ms": ceil["plan_stream_floor_us"][args.config] / 1e3,
+                         "stream_floor_frac": round(ceil["plan_stream_floor_us"][args.config]
+                                                    / 1e3 / kern["estimate"], 4),
+                         "stream_floor_source": ceil.get("plan_stream_source")}
+                        if est_path == "staged plan"
+                        and args.config in ceil.get("plan_stream_floor_us", {}) else {})},
     }
     dominant = max(("scan", "slide", "estimate"), key=lambda n: kern[n])
     roof = {"kernel": dominant, **{k: v for k, v in kernels[dominant].items() if k != "ms"}}
