@@ -52,6 +52,20 @@ namespace {
 #define VBDR_PLAN_SORT 0  // fill order: 0 register bank, 1 accumulator bank, 2 both (experiment)
 #endif
 
+#ifdef VBDR_PLAN_TRACE  // diagnostics build only (tools/plan_trace.py): per-CTA globaltimer stamps
+// [cta][phase][0..3] = consumer warp 0: wait-full start, wait-full end, release;
+// producer: wait-empty end (issue); [cta][64][0..3] = start, loop end (warp 0), finish end
+__device__ unsigned long long g_plan_trace[148][65][4];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PTRACE(ph, k) g_plan_trace[blockIdx.x % 148][(ph) < 64 ? (ph) : 64][k] = gtime()
+#else
+#define PTRACE(ph, k) ((void)0)
+#endif
+
 constexpr int kT = vbdr_launch::kPlanThreads;   // 512
 constexpr int kW = kT / 32;                     // 16 warps
 constexpr int kCap = vbdr_launch::kPlanEntCap;  // largest entries per (CTA, phase) buffer
@@ -476,6 +490,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
   __syncthreads();
   const uint32_t phases = pl.phases;
   const uint8_t *regs = e.regmax;
+  if (tid == 0) PTRACE(64, 0);
   if (w == kW) {  // producer
     if (lane == 0) {
       for (uint32_t ph = 0; ph < phases; ++ph) {
@@ -485,6 +500,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
           atomicAdd(err, 1ull);
           break;
         }
+        PTRACE(ph, 3);
         const uint64_t key = (uint64_t)p * phases + ph;
         const uint32_t e0 = pl.range_base[key], e1 = pl.range_base[key + 1];
         const uint32_t ebytes = (e1 - e0) * 4u;  // ranges are multiples of 32 entries
@@ -530,6 +546,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
     const uint32_t K = 1u << e.L;     // 2^(L - M) = K >> M
     for (uint32_t ph = 0; ph < phases; ++ph) {
       const int b = ph & 1;
+      if (w == 0 && lane == 0) PTRACE(ph, 0);
       if (!mbar_wait(&sm.full[b], (ph >> 1) & 1u)) {
         if (lane == 0) {
           atomicAdd(err, 1ull);
@@ -537,6 +554,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
         }
         break;
       }
+      if (w == 0 && lane == 0) PTRACE(ph, 1);
       const uint8_t *tab = sm.tab[b];
       const uint32_t r0 = sm.start[b][w], r1 = sm.start[b][w + 1];
       const uint32_t *ent = sm.ent[b] + lane;
@@ -563,10 +581,12 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
         add(v, tab[v & (BLOCK - 1u)]);
       }
       __syncwarp();
+      if (w == 0 && lane == 0) PTRACE(ph, 2);
       if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(&sm.empty[b])) : "memory");
     }
   }
   __syncthreads();
+  if (tid == 0) PTRACE(64, 1);
   pdl_trigger();
   const double etot_z = SUMS ? 0.0 : sm.etot_z;
   // accumulator index (slot, lane) of warp w <-> q = slot 512 + lane 16 + w
@@ -583,6 +603,10 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
     plan_finish<SUMS>(e, h, acc[ss * 32u + ll], acc[accw + ss * 32u + ll], HLL, etot_z, out, outS,
                       outV);
   }
+#ifdef VBDR_PLAN_TRACE
+  __syncthreads();
+  if (tid == 0) PTRACE(64, 2);
+#endif
 }
 
 template <int BL>
@@ -650,6 +674,14 @@ cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, 
   k_plan_sched<<<(uint32_t)nkeys, kT, kW * 2048, s>>>(a, range_size_scratch);
   return cudaGetLastError();
 }
+
+#ifdef VBDR_PLAN_TRACE
+}  // namespace vbdr_launch
+extern "C" int vbdr_debug_plan_trace(unsigned long long *host, unsigned long long bytes) {
+  return (int)cudaMemcpyFromSymbol(host, g_plan_trace, bytes < sizeof(g_plan_trace) ? bytes : sizeof(g_plan_trace));
+}
+namespace vbdr_launch {
+#endif
 
 cudaError_t estimate_plan(const EstParams &e, const PlanLayout &pl, uint64_t n, double *out,
                           unsigned long long *outS, uint32_t *outV, cudaStream_t s) {
