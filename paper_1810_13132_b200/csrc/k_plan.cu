@@ -88,13 +88,15 @@ struct BuildArgs {
   uint32_t *range_base;  // [P * phases + 1], in entries
   uint32_t *entries;
   uint32_t *max_range;   // scalar
+  uint32_t hpc;          // hosts per CTA, ceil(n / P)
 };
 
-// Host h -> CTA p = h % P; q = h / P -> warp q % 16, lane (q / 16) % 32,
-// slot q / 512: short host lists still use every CTA and warp.  The host's
-// accumulator index in its warp is slot * 32 + lane.
-__host__ __device__ __forceinline__ uint64_t host_of(uint32_t p, uint64_t q, uint32_t P) {
-  return q * P + p;
+// Host h -> CTA p = h / hpc, q = h % hpc -> lane q % 32, warp (q / 32) % 16,
+// slot q / 512; the host's accumulator index in its warp is slot * 32 + lane.
+// A warp's 32 lanes hold 32 consecutive hosts of one slot, so the finish of
+// a slot writes 256 contiguous bytes.
+__host__ __device__ __forceinline__ uint64_t host_of(uint32_t p, uint64_t q, uint32_t hpc) {
+  return (uint64_t)p * hpc + q;
 }
 
 // (host, i) -> key = (CTA, phase), warp, bank of the register in the block,
@@ -102,10 +104,10 @@ __host__ __device__ __forceinline__ uint64_t host_of(uint32_t p, uint64_t q, uin
 __device__ __forceinline__ void locate_entry(const BuildArgs &a, uint64_t h, uint32_t i,
                                              uint64_t &key, uint32_t &warp, uint32_t &bank,
                                              uint32_t &val) {
-  const uint32_t p = (uint32_t)(h % a.P);
-  const uint64_t q = h / a.P;
-  warp = (uint32_t)(q % kW);
-  const uint32_t lane = (uint32_t)((q / kW) % 32u);
+  const uint32_t p = (uint32_t)(h / a.hpc);
+  const uint64_t q = h % a.hpc;
+  const uint32_t lane = (uint32_t)(q & 31u);
+  warp = (uint32_t)((q >> 5) % kW);
   const uint32_t slot = (uint32_t)(q / kT);
   const uint32_t s1 = fmix32(i ^ a.A0);                            // Alg.3
   const uint32_t pidx = fmix32(__ldg(a.hosts + h) ^ s1) & a.mask;  // Alg.3
@@ -383,10 +385,18 @@ __global__ void __launch_bounds__(kT) k_plan_sched(BuildArgs a, const uint32_t *
 
 // --------------------------------------------------------------- estimate
 __device__ __forceinline__ double hll_finish(double agg, double D, double lc, uint64_t V,
-                                             double s) {
+                                             double s, const double *lct = nullptr) {
   double E = __ddiv_rn(agg, D);
-  if (E <= lc && V > 0) E = __dmul_rn(s, log(__ddiv_rn(s, (double)V)));
+  // linear counting: s ln(s / V), from the plan's table of the same values
+  // (k_plan_lct) when there is one -- bit-identical, without a log per host
+  if (E <= lc && V > 0) E = __dmul_rn(s, lct ? __ldg(lct + V) : log(__ddiv_rn(s, (double)V)));
   return E;
+}
+
+// lct[V] = ln(g / V) for V = 1..g, computed exactly as hll_finish would
+__global__ void k_plan_lct(double *lct, uint32_t g) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v <= g; v += gridDim.x * blockDim.x)
+    lct[v] = v ? log(__ddiv_rn((double)g, (double)v)) : 0.0;
 }
 
 template <int BLOCK_LOG2>
@@ -420,7 +430,8 @@ __device__ __forceinline__ bool mbar_wait(uint64_t *bar, uint32_t parity) {
 template <bool SUMS>
 __device__ __forceinline__ void plan_finish(const EstParams &e, uint64_t h, uint32_t Sp, uint32_t V,
                                             bool HLL, double etot_z, double *out,
-                                            unsigned long long *outS, uint32_t *outV) {
+                                            unsigned long long *outS, uint32_t *outV,
+                                            const double *lct) {
   const unsigned long long S = Sp + (HLL ? (unsigned long long)V << e.L : 0ull);
   if constexpr (SUMS) {
     outS[h] = S;
@@ -429,11 +440,12 @@ __device__ __forceinline__ void plan_finish(const EstParams &e, uint64_t h, uint
     const double g = (double)e.g;
     double Es;
     if (e.est == 0u) {
-      Es = hll_finish(e.agg, __dmul_rn((double)S, e.inv2L), e.lc_g, V, g);
+      Es = hll_finish(e.agg, __dmul_rn((double)S, e.inv2L), e.lc_g, V, g, lct);
     } else {
       Es = __dmul_rn(e.coef_g, exp2(__ddiv_rn((double)S, g)));
     }
-    const double est = __dmul_rn(e.C, __dsub_rn(__ddiv_rn(Es, g), etot_z));
+    // g is a power of two: Es / g is exact as Es * (1 / g)
+    const double est = __dmul_rn(e.C, __dsub_rn(__dmul_rn(Es, __drcp_rn(g)), etot_z));
     out[h] = est > 0.0 ? est : 0.0;
   }
 }
@@ -465,7 +477,7 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
   const uint32_t accw = pl.st_slots * 32u + 32u;
   uint32_t *acc_all = reinterpret_cast<uint32_t *>(raw + sizeof(PlanSmem<BLOCK_LOG2>));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t P = gridDim.x, p = blockIdx.x;
+  const uint32_t p = blockIdx.x;
   if (w < kW) {
     for (uint32_t i = lane; i < 2u * accw; i += 32u) acc_all[w * 2u * accw + i] = 0u;
   }
@@ -584,29 +596,27 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
       if (w == 0 && lane == 0) PTRACE(ph, 2);
       if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(&sm.empty[b])) : "memory");
     }
-  }
-  __syncthreads();
-  if (tid == 0) PTRACE(64, 1);
-  pdl_trigger();
-  const double etot_z = SUMS ? 0.0 : sm.etot_z;
-  // accumulator index (slot, lane) of warp w <-> q = slot 512 + lane 16 + w
-  const uint32_t qn = pl.st_slots * (uint32_t)kT;
-  for (uint32_t q = tid; q < qn; q += blockDim.x) {
-    const uint64_t h = host_of(p, q, P);
-    if (h >= n) continue;  // (a CTA that timed out still writes its hosts: NaN)
-    const uint32_t ww = q % kW, ll = (q / kW) % 32u, ss = q / kT;
-    const uint32_t *acc = acc_all + ww * 2u * accw;
-    if (!sm.ok) {
-      plan_poison<SUMS>(h, out, outS, outV);
-      continue;
+    if (w == 0 && lane == 0) PTRACE(64, 1);
+    pdl_trigger();
+    // this warp's hosts are final once its last block is done (only this
+    // warp adds into them): finish them now, beside the other warps' last
+    // rounds -- slot s holds hosts q = s 512 + w 32 + lane of this CTA
+    const double etot_z = SUMS ? 0.0 : sm.etot_z;
+    for (uint32_t ss = 0; ss < pl.st_slots; ++ss) {
+      const uint32_t q = ss * (uint32_t)kT + (uint32_t)w * 32u + (uint32_t)lane;
+      const uint64_t h = host_of(p, q, pl.st_hpc);
+      if (q >= pl.st_hpc || h >= n) break;
+      if (!sm.ok) {  // (a CTA that timed out still writes its hosts: NaN)
+        plan_poison<SUMS>(h, out, outS, outV);
+        continue;
+      }
+      plan_finish<SUMS>(e, h, acc[ss * 32u + lane], acc[accw + ss * 32u + lane], HLL, etot_z, out,
+                        outS, outV, pl.lct);
     }
-    plan_finish<SUMS>(e, h, acc[ss * 32u + ll], acc[accw + ss * 32u + ll], HLL, etot_z, out, outS,
-                      outV);
-  }
 #ifdef VBDR_PLAN_TRACE
-  __syncthreads();
-  if (tid == 0) PTRACE(64, 2);
+    if (w == 0 && lane == 0) PTRACE(64, 2);
 #endif
+  }
 }
 
 template <int BL>
@@ -652,6 +662,7 @@ cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, 
   a.phases = pl.phases;
   a.P = pl.ctas;
   a.slots = pl.st_slots;
+  a.hpc = pl.st_hpc;
   a.counts = pl.counts;
   a.starts = pl.starts;
   a.range_base = pl.range_base;
@@ -672,6 +683,12 @@ cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, 
   e = cudaFuncSetAttribute(k_plan_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, kW * 2048);
   if (e != cudaSuccess) return e;
   k_plan_sched<<<(uint32_t)nkeys, kT, kW * 2048, s>>>(a, range_size_scratch);
+  if (pl.lct) k_plan_lct<<<(g + 256) / 256, 256, 0, s>>>(const_cast<double *>(pl.lct), g);
+  return cudaGetLastError();
+}
+
+cudaError_t plan_lct(const double *lct, uint32_t g, cudaStream_t s) {
+  k_plan_lct<<<(g + 256) / 256, 256, 0, s>>>(const_cast<double *>(lct), g);
   return cudaGetLastError();
 }
 

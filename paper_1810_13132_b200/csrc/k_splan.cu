@@ -182,16 +182,19 @@ __global__ void __launch_bounds__(32) k_sp_pad(SpBuild a) {
 
 // --------------------------------------------------------------- estimate
 __device__ __forceinline__ double hll_finish(double agg, double D, double lc, uint64_t V,
-                                             double s) {
+                                             double s, const double *lct = nullptr) {
   double E = __ddiv_rn(agg, D);
-  if (E <= lc && V > 0) E = __dmul_rn(s, log(__ddiv_rn(s, (double)V)));
+  // linear counting from the plan's table of s ln(s / V)'s logs (k_plan_lct,
+  // the same values) when there is one
+  if (E <= lc && V > 0) E = __dmul_rn(s, lct ? __ldg(lct + V) : log(__ddiv_rn(s, (double)V)));
   return E;
 }
 
 template <bool SUMS>
 __device__ __forceinline__ void sp_finish(const EstParams &e, uint64_t h, uint64_t Sp, uint32_t V,
                                           bool hll, double etot_z, double *out,
-                                          unsigned long long *outS, uint32_t *outV) {
+                                          unsigned long long *outS, uint32_t *outV,
+                                          const double *lct) {
   // HLL: S = S' + V 2^L (each zero register adds 2^(L - 0))
   const unsigned long long S = Sp + (hll ? (unsigned long long)V << e.L : 0ull);
   if constexpr (SUMS) {
@@ -201,11 +204,12 @@ __device__ __forceinline__ void sp_finish(const EstParams &e, uint64_t h, uint64
     const double g = (double)e.g;
     double Es;
     if (hll) {
-      Es = hll_finish(e.agg, __dmul_rn((double)S, e.inv2L), e.lc_g, V, g);
+      Es = hll_finish(e.agg, __dmul_rn((double)S, e.inv2L), e.lc_g, V, g, lct);
     } else {
       Es = __dmul_rn(e.coef_g, exp2(__ddiv_rn((double)S, g)));
     }
-    const double est = __dmul_rn(e.C, __dsub_rn(__ddiv_rn(Es, g), etot_z));
+    // g is a power of two: Es / g is exact as Es * (1 / g)
+    const double est = __dmul_rn(e.C, __dsub_rn(__dmul_rn(Es, __drcp_rn(g)), etot_z));
     out[h] = est > 0.0 ? est : 0.0;
   }
 }
@@ -322,7 +326,7 @@ k_estimate_sp(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out,
   if (pl.sp_C == 1) {
     for (uint32_t slot = threadIdx.x; slot < hpg; slot += kT) {
       const uint64_t h = (uint64_t)slot * P + p;
-      if (h < n) sp_finish<SUMS>(e, h, Sacc[slot], Vacc[slot], HLL, s_etot_z, out, outS, outV);
+      if (h < n) sp_finish<SUMS>(e, h, Sacc[slot], Vacc[slot], HLL, s_etot_z, out, outS, outV, pl.lct);
     }
     return;
   }
@@ -352,7 +356,7 @@ k_estimate_sp(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out,
       Sp += x & 0xFFFFFFFFull;
       V += (uint32_t)(x >> 32);
     }
-    sp_finish<SUMS>(e, h, Sp, V, HLL, s_etot_z, out, outS, outV);
+    sp_finish<SUMS>(e, h, Sp, V, HLL, s_etot_z, out, outS, outV, pl.lct);
   }
   if (threadIdx.x == 0) pl.sp_gcount[p] = 0u;  // ready for the next launch on this plan
 }

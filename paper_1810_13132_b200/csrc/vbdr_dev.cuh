@@ -232,7 +232,9 @@ struct PlanLayout {
   uint32_t *entries;
   uint32_t *max_range;   // build: largest (CTA, block) entry count
   unsigned long long *error;  // estimate: set if a staged transfer never landed
+  const double *lct;     // kinds 0, 2: ln(g / V) for V = 0..g (linear counting), or null
   uint32_t st_slots;     // kind 0: accumulator slots per lane (hosts per thread)
+  uint32_t st_hpc;       // kind 0: hosts per CTA (host h -> CTA h / st_hpc)
   // kind 2 (sorted plan); counts = bucket cursors, range_size = segment totals
   uint32_t sp_C;           // register ranges per host group
   uint32_t sp_hpg;         // accumulator slots per group (hosts / P, rounded up)
@@ -245,6 +247,7 @@ struct PlanLayout {
   uint32_t *sp_gcount;     // [P] arrivals per group (C > 1)
 };
 size_t plan_smem_bytes(uint32_t block_log2, uint32_t slots);  // 0: unsupported block
+cudaError_t plan_lct(const double *lct, uint32_t g, cudaStream_t s);  // fill a plan's log table
 cudaError_t plan_build(const PlanLayout &pl, const uint32_t *hosts, uint64_t n, uint32_t g,
                        uint32_t A0, uint32_t mask, uint32_t *range_size_scratch, cudaStream_t s);
 cudaError_t estimate_plan(const EstParams &e, const PlanLayout &pl, uint64_t n, double *out,

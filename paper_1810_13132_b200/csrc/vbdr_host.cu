@@ -270,9 +270,9 @@ void decode_ages(const vbdr *h, WordAt word, int mode, uint16_t *out) {
 // accumulators (hosts / SMs per CTA) fit shared memory and whose expected
 // entries per (CTA, block) stay well inside a stage.
 struct PlanGeom {
-  uint32_t ctas, phases, block_log2, slots;
-  uint64_t nkeys, off_range_base, off_starts, off_counts, off_range_size, off_misc, off_entries,
-      bytes;
+  uint32_t ctas, phases, block_log2, slots, hpc;
+  uint64_t nkeys, off_range_base, off_starts, off_counts, off_range_size, off_misc, off_lct,
+      off_entries, bytes;
 };
 
 bool plan_geom(const vbdr *h, uint64_t n_hosts, PlanGeom *g) {
@@ -307,6 +307,7 @@ bool plan_geom(const vbdr *h, uint64_t n_hosts, PlanGeom *g) {
   if (!found) return false;
   g->ctas = (uint32_t)sms;
   g->slots = (uint32_t)slots;
+  g->hpc = (uint32_t)hpc;
   g->phases = (uint32_t)(z >> g->block_log2);
   g->nkeys = (uint64_t)g->ctas * g->phases;
   uint64_t off = 0;
@@ -320,6 +321,7 @@ bool plan_geom(const vbdr *h, uint64_t n_hosts, PlanGeom *g) {
   g->off_counts = take(4 * g->nkeys * vbdr_launch::kPlanThreads);
   g->off_range_size = take(4 * g->nkeys);
   g->off_misc = take(64);
+  g->off_lct = take(8ull * (h->cfg.m + 1));  // linear-counting log table
   // every (CTA, block, warp) group is padded to whole rounds of 32 entries
   const uint64_t groups = g->nkeys * (vbdr_launch::kPlanThreads / 32);
   g->off_entries = take(4 * (n_hosts * h->cfg.m + 31 * groups));
@@ -341,6 +343,8 @@ vbdr_launch::PlanLayout plan_layout(const PlanGeom &g, void *d_plan, uint64_t n_
   pl.max_range = reinterpret_cast<uint32_t *>(b + g.off_misc);
   pl.error = reinterpret_cast<unsigned long long *>(b + g.off_misc + 8);
   pl.st_slots = g.slots;
+  pl.lct = reinterpret_cast<const double *>(b + g.off_lct);
+  pl.st_hpc = g.hpc;
   pl.entries = reinterpret_cast<uint32_t *>(b + g.off_entries);
   return pl;
 }
@@ -706,7 +710,7 @@ vbdr_status vbdr_select_above(vbdr_t *h, const double *d_est, uint64_t n, double
 struct SpGeom {
   uint32_t ctas, C, P, hpg, SB, range_log2, seg_log2, nseg;
   uint64_t nbuckets, nkeys, off_offs, off_segtot, off_segbase, off_part, off_gcount, off_misc,
-      off_entries, bytes;
+      off_lct, off_entries, bytes;
 };
 
 bool sp_geom(const vbdr *h, uint64_t n_hosts, SpGeom *g) {
@@ -757,6 +761,7 @@ bool sp_geom(const vbdr *h, uint64_t n_hosts, SpGeom *g) {
     g->off_part = take(C > 1 ? 8ull * sms * hpg : 8);
     g->off_gcount = take(4ull * P);
     g->off_misc = take(64);
+    g->off_lct = take(8ull * (h->cfg.m + 1));
     g->off_entries = take(4 * (n_hosts * h->cfg.m + 31 * nkeys));
     g->bytes = off;
     return true;
@@ -776,6 +781,7 @@ vbdr_launch::PlanLayout sp_layout(const SpGeom &g, void *d_plan, uint64_t n_host
   pl.sp_part = reinterpret_cast<unsigned long long *>(b + g.off_part);
   pl.sp_gcount = reinterpret_cast<uint32_t *>(b + g.off_gcount);
   pl.error = reinterpret_cast<unsigned long long *>(b + g.off_misc);
+  pl.lct = reinterpret_cast<const double *>(b + g.off_lct);
   pl.entries = reinterpret_cast<uint32_t *>(b + g.off_entries);
   pl.sp_C = g.C;
   pl.sp_hpg = g.hpg;
@@ -863,6 +869,7 @@ vbdr_status vbdr_plan_build_kind(vbdr_t *h, const uint32_t *d_hosts, uint64_t n_
                                           pl.error, cs);
     if (e == cudaSuccess)
       e = vbdr_launch::sp_fill(pl, d_hosts, n_hosts, h->cfg.m, h->p.A0, h->p.mask, cs);
+    if (e == cudaSuccess) e = vbdr_launch::plan_lct(pl.lct, h->cfg.m, cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) return cuda_fail(h, e, "plan_build");
     h->info.launches += 5;

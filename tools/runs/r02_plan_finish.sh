@@ -1,0 +1,5 @@
+# per-warp finish + block host mapping (coalesced output), caida staged
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -k "plan or e2e_pipelined or query_top or random_config" -q -x > gpurun_out/pytest_fin.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_fin.log
+A="--estimate staged --no-e2e --no-cpu-baseline --steps 30 --warmup 5"
+TAG=fin bash tools/ab.sh "$A" main main
+cp tools/var_build/trace/libvbdr.so paper_1810_13132_b200/_lib/libvbdr.so && python tools/plan_trace.py 2>&1 | tail -7
