@@ -488,16 +488,6 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     sm.ok = 1u;
-    if (!SUMS) {
-      const unsigned long long St = e.acc[0], Vt = e.acc[1];
-      double Et;
-      if (e.est == 0u) {
-        Et = hll_finish(e.azz, __dmul_rn((double)St, e.inv2L), e.lc_z, Vt, e.z);
-      } else {
-        Et = __dmul_rn(e.coef_z, exp2(__ddiv_rn((double)St, e.z)));
-      }
-      sm.etot_z = __ddiv_rn(Et, e.z);
-    }
   }
   __syncthreads();
   const uint32_t phases = pl.phases;
@@ -507,6 +497,19 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
     if (lane == 0) {
       for (uint32_t ph = 0; ph < phases; ++ph) {
         const int b = ph & 1;
+        if (ph == (phases > 2u ? 2u : 0u) && !SUMS) {
+          // the pool's own estimate E_tot / z for the noise subtraction, off the
+          // first stages' critical path: the consumers read it in their finish,
+          // after waiting on a stage this lane armed later (release / acquire)
+          const unsigned long long St = e.acc[0], Vt = e.acc[1];
+          double Et;
+          if (e.est == 0u) {
+            Et = hll_finish(e.azz, __dmul_rn((double)St, e.inv2L), e.lc_z, Vt, e.z);
+          } else {
+            Et = __dmul_rn(e.coef_z, exp2(__ddiv_rn((double)St, e.z)));
+          }
+          sm.etot_z = __ddiv_rn(Et, e.z);
+        }
         // buffer b last held phase ph - 2: wait for its (ph/2 - 1)-th release
         if (ph >= 2 && !mbar_wait(&sm.empty[b], ((ph >> 1) + 1u) & 1u)) {
           atomicAdd(err, 1ull);
