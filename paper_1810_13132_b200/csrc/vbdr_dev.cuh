@@ -201,11 +201,8 @@ struct EstParams {
 // register block, warp) rounds of 32 entries.  Layout of the caller's plan buffer.
 constexpr int kPlanThreads = 512;
 constexpr int kPlanEntCap = 8192; // entries per (CTA, block) staged in shared memory, 2^16 blocks
-// stage capacity for blocks of 2^bl registers: the entries per block scale
-// with the block, the round padding (up to 16 warps x 31 entries) does not
-constexpr uint32_t plan_ent_cap(uint32_t bl) {
-  return bl >= 16 ? (uint32_t)kPlanEntCap : ((uint32_t)kPlanEntCap >> (16 - bl)) + 1024u;
-}
+// entry stage capacity (entries per (CTA, block) stage), every block size
+constexpr uint32_t plan_ent_cap(uint32_t) { return (uint32_t)kPlanEntCap; }
 constexpr int kPlanStride = 20;   // round starts per (CTA, block): 16 warps + total, 16-byte padded
 // Sorted plan (k_splan.cu): entries sorted by register line, P host groups x
 // C register ranges, one CTA per SM.
