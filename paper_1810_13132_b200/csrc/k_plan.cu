@@ -426,6 +426,14 @@ __device__ __forceinline__ bool mbar_wait(uint64_t *bar, uint32_t parity) {
   return true;
 }
 
+// The zero count V from the accumulators: HLL adds 2^L per zero register,
+// so the word holds V 2^L mod 2^32, which wraps only for V = g when g 2^L =
+// 2^32, i.e. every register zero -- exactly when S' = 0 (each M >= 1 adds >= 1).
+__device__ __forceinline__ uint32_t plan_zero_count(uint32_t Sp, uint32_t Vz, bool HLL,
+                                                    const EstParams &e) {
+  return HLL ? (Sp == 0u ? e.g : Vz >> e.L) : Vz;
+}
+
 // One host's fp64 finish from its integer sums (k_estimate's operation order).
 template <bool SUMS>
 __device__ __forceinline__ void plan_finish(const EstParams &e, uint64_t h, uint32_t Sp, uint32_t V,
@@ -577,7 +585,10 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
       // atomics.  One atomic per lane: M >= 1 adds its term to S', M = 0 adds
       // 1 to V
       auto add = [&](uint32_t v, uint32_t M) {
-        const uint32_t cv = M == 0u ? 1u : (HLL ? K >> M : M);
+        // HLL: 2^(L - M) = K >> M for every M, the zero count included (it
+        // holds V 2^L mod 2^32; plan_zero_count recovers V) -- one shift, no
+        // select; LogLog / PCSA: M into S', 1 into the zero count
+        const uint32_t cv = HLL ? K >> M : (M == 0u ? 1u : M);
         const uint32_t addr = acc_base + (v >> 16) + (M == 0u ? vofs : 0u);
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(cv) : "memory");
       };
@@ -613,7 +624,9 @@ k_estimate_plan(EstParams e, PlanLayout pl, uint64_t n, double *__restrict__ out
         plan_poison<SUMS>(h, out, outS, outV);
         continue;
       }
-      plan_finish<SUMS>(e, h, acc[ss * 32u + lane], acc[accw + ss * 32u + lane], HLL, etot_z, out,
+      plan_finish<SUMS>(e, h, acc[ss * 32u + lane],
+                        plan_zero_count(acc[ss * 32u + lane], acc[accw + ss * 32u + lane], HLL, e),
+                        HLL, etot_z, out,
                         outS, outV, pl.lct);
     }
 #ifdef VBDR_PLAN_TRACE
