@@ -609,6 +609,37 @@ def test_abi_errors():
     assert pool.estimate(torch.zeros(0, dtype=torch.int32, device=DEV)).numel() == 0
 
 
+@pytest.mark.parametrize("kind", ["staged", "sorted"])
+def test_plan_estimate_all_zero_registers(kind):
+    """Hosts whose registers are all zero (a fresh pool, and every host after
+    the window has passed with empty slices): the staged plan's zero count
+    holds V 2^L mod 2^32, which wraps to 0 exactly then (V = g, S' = 0).
+    Sums and estimates equal the gather kernel's and the oracle's."""
+    tr = synth.CONFIGS["tiny"]
+    cfg = oracle.PoolConfig(b=5, k=4, z=1 << 12)
+    ref = oracle.Pool(cfg, "serial")
+    pool = VBDR(32, 4, 1 << 12, device=DEV)
+    hosts_np = tr.host_ids()
+    hosts = dev_u32(hosts_np)
+    plan = pool.plan(hosts, kind=kind)
+    empty = np.zeros((0, 2), np.uint32)
+    for t, pairs in enumerate([empty, synth.generate(tr, 1), empty, empty, empty, empty, empty]):
+        if len(pairs):
+            pool.scan_slice(dev_u32(pairs))
+        pool.slide()
+        ref.slice(pairs)
+        S1, V1 = pool.host_sums_plan(plan)
+        S2, V2 = pool.host_sums(hosts)
+        assert torch.equal(S1, S2) and torch.equal(V1, V2)
+        a = pool.estimate_plan(plan).cpu().numpy()
+        assert np.array_equal(a, pool.estimate(hosts).cpu().numpy())
+        M = ref.readout()
+        if not M.any():  # every register zero: V = g for every host
+            assert (V1.cpu().numpy() == 32).all()
+        check_estimates(a, ref.estimate(M, hosts_np), est_floor(ref, M, hosts_np))
+    pool.plan_check(plan)
+
+
 def test_plan_abi_errors():
     """Plan calls fail loudly and launch nothing: a plan of another handle, a
     released plan, a buffer too small or misaligned, an unknown kind."""
