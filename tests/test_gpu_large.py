@@ -131,3 +131,11 @@ def test_bigwin_full_size_multipass_estimate():
     """2^28 BDRs: the estimate runs in 4 passes over 64 MiB register ranges."""
     inf = run_large("bigwin", 256, 60, 1 << 28, 3, plan_kinds=("sorted", "passid"))
     assert inf["zbits"] == 6 and inf["words"] == 5
+
+
+def test_10G_full_size_packed():
+    """Layout P (gsmall semantics) at full 10G size past k slices: registers
+    against the window's rebuild, pool and host sums, every plan estimate
+    bit-identical to the gather, sampled hosts against the oracle."""
+    inf = run_large("10G", 256, 10, 1 << 26, 12, layout="packed")
+    assert inf["zbits"] == 4
