@@ -139,3 +139,9 @@ def test_10G_full_size_packed():
     bit-identical to the gather, sampled hosts against the oracle."""
     inf = run_large("10G", 256, 10, 1 << 26, 12, layout="packed")
     assert inf["zbits"] == 4
+
+
+def test_10G_full_size_stamps():
+    """Layout S (per-(BDR, rank) u32 stamps, 6 GiB at 10G) at full size past k
+    slices: registers against the window's rebuild, sums, plan estimates."""
+    run_large("10G", 256, 10, 1 << 26, 12, layout="stamps")
